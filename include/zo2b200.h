@@ -1,0 +1,204 @@
+/*
+ * zo2b200.h -- C ABI of the B200 (sm_100a) ZO2 step library
+ * (paper_2503_12668_b200/_lib/libzo2b200.so).
+ *
+ * The reference (zo2lab, /root/reference/pkg/src/zo2lab) is pure NumPy and
+ * has no FFI; each entry point below replaces one computation of its
+ * Python hot path, cited as file:line.  Conventions:
+ *   - every function returns 0 (ZO2_OK) or a ZO2_E_* status; the Python host
+ *     maps statuses onto the reference's exception taxonomy (errors.py:4-21);
+ *     zo2_last_error() returns a message for the last failure.
+ *   - device pointers are plain pointers allocated by the caller (torch);
+ *     `stream` is a cudaStream_t passed as void*; nothing here allocates on
+ *     the hot path and nothing synchronises unless its name ends in _sync.
+ *   - host-side functions (zo2_host_*) touch host memory only.
+ *   - element formats: ZO2_F64, ZO2_F32, ZO2_F16, ZO2_BF16, ZO2_F8E4M3 follow
+ *     numerics.py:48-84 (ElemFormat); low-bit formats are storage only.
+ */
+#ifndef ZO2B200_H
+#define ZO2B200_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py:4-21) ---- */
+#define ZO2_OK 0
+#define ZO2_E_ARG 1          /* UsageError / ValueError               */
+#define ZO2_E_CUDA 2         /* CUDA runtime failure (RuntimeError)   */
+#define ZO2_E_CAPACITY 3     /* CapacityError                         */
+#define ZO2_E_SCHED 4        /* SchedulingContractError               */
+#define ZO2_E_STATE 5        /* StateCorruptionError                  */
+#define ZO2_E_NONFINITE 6    /* NonFiniteLossError                    */
+#define ZO2_E_UNSUPPORTED 7  /* shape/format outside the kernels' set */
+
+/* ---- element formats (numerics.py:48-84) ---- */
+#define ZO2_F64 0
+#define ZO2_F32 1
+#define ZO2_F16 2
+#define ZO2_BF16 3
+#define ZO2_F8E4M3 4
+
+/* ---- RNG stream ids (numerics.py:42-45) ---- */
+#define ZO2_PERTURB_STREAM 0
+#define ZO2_BATCH_STREAM 1
+#define ZO2_INIT_STREAM 2
+#define ZO2_DATA_STREAM 3
+
+const char *zo2_last_error(void);
+int zo2_version(void);
+/* number of kernel launches issued by this library since load (evidence for
+ * bench.py's gpu_launches) */
+uint64_t zo2_launch_count(void);
+
+/* ======================= K1: counter-based Gaussian direction =========== */
+/* numerics.py:171-182 gaussian_fill(RngState(seed, stream, counter), n):
+ * out[i] = ndtri(((raw(counter+i) >> 11) + 0.5) * 2^-53), bit-exact. */
+int zo2_z_fill(double *out, uint64_t n, uint64_t seed, uint64_t stream,
+               uint64_t counter, void *cuda_stream);
+/* numerics.py:161-168 raw_uint64. */
+int zo2_raw_fill(uint64_t *out, uint64_t n, uint64_t seed, uint64_t stream,
+                 uint64_t counter, void *cuda_stream);
+/* Host restatements of the same generator (same source as the device code;
+ * used by the host runtime for batch sampling, model.py:198-224 init is on
+ * device). */
+int zo2_host_raw_u64(uint64_t *out, uint64_t n, uint64_t seed,
+                     uint64_t stream, uint64_t counter);
+int zo2_host_gaussian_fill(double *out, uint64_t n, uint64_t seed,
+                           uint64_t stream, uint64_t counter);
+uint64_t zo2_host_derive_step_seed(uint64_t base_seed, uint64_t step_index);
+
+/* model.py:198-224 init_params, one segment: out = fmt(std * z) with z drawn
+ * at (seed, INIT_STREAM, counter); fmt is ZO2_F32 or ZO2_F64. */
+int zo2_init_normal(void *out, int fmt, uint64_t n, double std, uint64_t seed,
+                    uint64_t counter, void *cuda_stream);
+int zo2_fill_const(void *out, int fmt, uint64_t n, double value,
+                   void *cuda_stream);
+
+/* ======================= K2: perturb / update ============================ */
+/* model.py:227-233 axpy with regenerated z (zo_ref.py:59-74 perturb_all for
+ * one bucket; zo2_engine.py:161-174 _perturb / _update_flat):
+ *   w[i] = store(f64(w[i]) + coef * z(seed, stream, counter + i)).
+ * fmt is ZO2_F32 or ZO2_F64. */
+int zo2_axpy_z(void *w, int fmt, uint64_t n, double coef, uint64_t seed,
+               uint64_t stream, uint64_t counter, void *cuda_stream);
+
+/* Operand emission for one bucket segment during the fused update+perturb
+ * (the dual forward's W+eps*z and W-eps*z). */
+#define ZO2_OUT_NONE 0
+#define ZO2_OUT_F32 1        /* f32 copy, same layout (vectors: LN g/b, biases) */
+#define ZO2_OUT_BF16_T 2     /* bf16, transposed to [cols, rows] (K-major B)   */
+#define ZO2_OUT_SPLIT_T 3    /* bf16 hi + bf16 lo planes, transposed           */
+#define ZO2_OUT_BF16 4       /* bf16, same layout ([rows, cols] already K-major) */
+#define ZO2_OUT_SPLIT 5      /* bf16 hi + lo planes, same layout               */
+typedef struct zo2_segment_desc {
+  uint64_t offset;       /* element offset in the bucket (= RNG offset)   */
+  uint32_t rows, cols;   /* row-major segment shape; vectors rows = 1     */
+  int32_t out_kind;      /* ZO2_OUT_*                                     */
+  int32_t pad_;
+  void *out_plus;        /* W + eps z   (hi plane for split kinds)        */
+  void *out_minus;       /* W - eps z                                     */
+  void *out_plus_lo;     /* lo planes (split kinds only)                  */
+  void *out_minus_lo;
+} zo2_segment_desc;
+
+/* K2, fused per-module step arithmetic of zo2_engine.py:183-204 dual_forward:
+ *   if (update && *d_g != 0):  w = st(w + (-(lr * *d_g)) * z(lrs_seed, 0, base+i))
+ *   w+ = st(w + eps z(rs)); w- = st(w+ + (-2 eps) z(rs)); w = st(w- + eps z(rs))
+ * (each st() is one axpy rounding, model.py:233).  update = 2 applies the
+ * update without the g != 0 gate (naive update-after-forward,
+ * zo2_engine.py:251-260).  `arena` holds the module
+ * in `wire_fmt` (F64/F32, or a codec format decoded to F32 on read and
+ * encoded on write, runtime.py:172-184); arithmetic is f64 when wire_fmt is
+ * ZO2_F64 and f32 otherwise.  perturb=0 skips the +eps/-2eps/+eps sequence
+ * (naive-mode update pass, finalize drain).  codec conversions tally into
+ * d_conv_counts[0] (NaN) and [1] (saturated) if non-null (ConversionSummary,
+ * numerics.py:210-217). */
+int zo2_update_perturb(void *arena, int wire_fmt, uint64_t n, uint64_t base,
+                       int update, const double *d_g, double lr,
+                       uint64_t lrs_seed, int perturb, double eps,
+                       uint64_t rs_seed, const zo2_segment_desc *segs,
+                       int n_segs, uint64_t *d_conv_counts, void *cuda_stream);
+
+/* ======================= K9: wire codecs ================================= */
+/* numerics.py:281-311 encode/decode; fmt in {ZO2_F16, ZO2_BF16, ZO2_F8E4M3}. */
+int zo2_encode(const float *src, void *dst, int fmt, uint64_t n,
+               uint64_t *d_conv_counts, void *cuda_stream);
+int zo2_decode(const void *src, float *dst, int fmt, uint64_t n,
+               void *cuda_stream);
+
+/* ======================= K10: projected gradient ========================= */
+/* zo2_engine.py:239-246: l+- = sums[0|1] / count ; g = (l+ - l-) / (2 eps).
+ * Writes out[0]=l+, out[1]=l-, out[2]=g; out[2] is left at 0 and *d_flag=1
+ * when either loss is non-finite (NonFiniteLossError is raised by the host). */
+int zo2_form_g(const double *d_sums, double count, double eps, double *d_out,
+               int *d_flag, void *cuda_stream);
+
+/* ======================= forward kernels ================================= */
+/* model.py:251-261 forward_embedding for both signs, with the module's
+ * deferred update and perturbation recomputed for the gathered rows:
+ *   out+-[t, c] = f32(tok+-[ids[t], c] + pos+-[t % S, c]).
+ * `table` is the f32 embedding bucket ([V*d] tok then [S*d] pos) BEFORE this
+ * step's update; base is the bucket's RNG offset (0 in canonical order). */
+int zo2_embed_dual(const int64_t *ids, uint64_t n_tok, uint32_t seq,
+                   uint32_t dim, uint32_t vocab, uint32_t max_seq,
+                   const float *table, uint64_t base, int update,
+                   const double *d_g, double lr, uint64_t lrs_seed,
+                   double eps, uint64_t rs_seed, float *out_plus,
+                   float *out_minus, void *cuda_stream);
+
+/* model.py:241-244 _layer_norm (population variance, eps 1e-5) on f32 rows,
+ * writing a GEMM A operand: bf16 (lo == NULL) or bf16 hi+lo planes. */
+int zo2_layernorm(const float *x, uint64_t rows, uint32_t dim,
+                  const float *gamma, const float *beta, void *out_hi,
+                  void *out_lo, void *cuda_stream);
+
+/* f32 activations -> GEMM A operand (bf16, or bf16 hi+lo planes when lo != NULL). */
+int zo2_to_operand(const float *x, uint64_t n, void *out_hi, void *out_lo,
+                   void *cuda_stream);
+
+/* Generic sm_100a tcgen05 GEMM  C[M,N] = A[M,K] . B[N,K]^T  (both K-major
+ * bf16, fp32 accumulation in TMEM), batched over `batch` independent
+ * problems (the +eps and -eps forwards).  With split (A_lo, B_lo non-null)
+ * it computes A_hi.B_hi + A_hi.B_lo + A_lo.B_hi (f32-faithful 3-pass bf16).
+ * Epilogues (model.py:272-301):
+ *   ZO2_EPI_STORE      C = acc + bias                (f32 out)
+ *   ZO2_EPI_RESIDUAL   C += acc + bias               (f32 in/out, h + (x@W+b))
+ *   ZO2_EPI_GELU       C = gelu_erf(acc + bias) as an operand (bf16 / split)
+ *   ZO2_EPI_CE         cross-entropy partials of the head logits per
+ *                      (row, n-tile): max, sum exp, target logit  (model.py:304)
+ */
+#define ZO2_EPI_STORE 0
+#define ZO2_EPI_RESIDUAL 1
+#define ZO2_EPI_GELU 2
+#define ZO2_EPI_CE 3
+typedef struct zo2_gemm_problem {
+  const void *a_hi, *a_lo;   /* [M, K] bf16                               */
+  const void *b_hi, *b_lo;   /* [N, K] bf16                               */
+  const float *bias;         /* [N] f32 or NULL                           */
+  void *c;                   /* f32 [M, N] (STORE/RESIDUAL) / bf16 hi (GELU) */
+  void *c_lo;                /* GELU split lo plane                       */
+  const int64_t *targets;    /* CE: [M] target ids                        */
+  float *ce_part;            /* CE: [M, n_tiles_n, 3] partials            */
+} zo2_gemm_problem;
+int zo2_gemm(const zo2_gemm_problem *probs, int batch, uint32_t M, uint32_t N,
+             uint32_t K, int epilogue, void *cuda_stream);
+/* N-tile width the GEMM uses (CE partial count = ceil(N / tile)). */
+int zo2_gemm_tile_n(int split);
+
+/* Combine CE partials into per-problem token sums (f64): sums[b] =
+ * sum_t (logsumexp_t - logit_t[target_t])  (model.py:304-313 numerator). */
+int zo2_ce_reduce(const float *ce_part, uint32_t M, uint32_t n_tiles,
+                  int batch, uint64_t part_stride, double *d_sums,
+                  void *cuda_stream);
+
+/* model.py:273-283 causal softmax attention on packed qkv (f32 [B*S, 3d],
+ * heads split as reshape(B,S,H,hd)), writing ctx as an A operand. */
+int zo2_attention(const float *qkv, uint32_t batch, uint32_t seq,
+                  uint32_t n_heads, uint32_t head_dim, void *ctx_hi,
+                  void *ctx_lo, void *cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZO2B200_H */

@@ -1,0 +1,511 @@
+// zo2_gemm_sm100.cu -- K3: the dual-forward GEMMs on 5th-gen tensor cores.
+//
+//   C[M,N] = A[M,K] . B[N,K]^T     A, B bf16 K-major, fp32 accumulation in TMEM
+//
+// Persistent, warp-specialised kernel (one CTA per SM):
+//   warp 0      TMA producer (cp.async.bulk.tensor, 128B swizzle, mbarrier tx)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused epilogue
+// Two TMEM accumulators let the epilogue of tile i overlap the MMAs of i+1.
+// The +eps and -eps problems of the dual forward are one launch (batch = 2).
+//
+// SPLIT (f32 arithmetic, model.py f32 path): operands carry a bf16 hi and a
+// bf16 lo plane (x = hi + lo to ~2^-16) and every k-step issues
+// hi.hi + hi.lo + lo.hi, all into the same fp32 TMEM accumulator.
+//
+// Epilogues (model.py:272-301): bias store (qkv), bias + residual (attention
+// out-proj, MLP out), bias + erf-GELU emitted as the next GEMM's A operand
+// (mlp_in), and the cross-entropy partials of the LM head (model.py:304-313)
+// so the [T, V] logits never reach HBM.
+#include "zo2_common.cuh"
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
+#include <unordered_map>
+#include <string.h>
+#include <stdio.h>
+
+void zo2_count_launch(uint64_t n = 1);
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = one 128-byte swizzle row
+constexpr int NUM_THREADS = 192;
+
+struct alignas(64) GemmArgs {
+  CUtensorMap tm[2][4];  // [problem][a_hi, a_lo, b_hi, b_lo]
+  const float *bias[2];
+  void *c[2];
+  void *c_lo[2];
+  const int64_t *targets[2];
+  float *ce_part[2];
+  uint32_t M, N, K;
+  int batch;
+};
+
+// ---------------------------------------------------------------- PTX glue
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, uint64_t *bar,
+                                            int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)tm), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 lanes x 32 consecutive fp32 columns -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+        "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+        "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row atoms 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) |
+         ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// Instruction descriptor: bf16 x bf16 -> f32, both K-major, M = 128, N = n.
+__host__ __device__ constexpr uint32_t idesc_bf16(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ float gelu_erf(float x) {
+  return 0.5f * x * (1.0f + erff(x * 0.70710678118654752440f));
+}
+
+template <int BN, bool SPLIT>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = (SPLIT ? 2 : 1) * (A_BYTES + B_BYTES);
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN, bool SPLIT, int EPI>
+__global__ void __launch_bounds__(NUM_THREADS, 1) k_gemm(const __grid_constant__ GemmArgs args) {
+  using C = Cfg<BN, SPLIT>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = (uint64_t *)(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t *empty = full + C::STAGES;
+  uint64_t *tfull = empty + C::STAGES;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t M = args.M, N = args.N, K = args.K;
+  const uint32_t tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  const uint32_t tiles = tiles_m * tiles_n * (uint32_t)args.batch;
+  const uint32_t kblocks = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    for (int p = 0; p < args.batch; ++p)
+      for (int j = 0; j < 4; ++j)
+        if (SPLIT || (j & 1) == 0)
+          asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&args.tm[p][j]) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"((uint32_t)C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const uint32_t p = t / (tiles_m * tiles_n);
+        const uint32_t r = t % (tiles_m * tiles_n);
+        const int m0 = (int)((r / tiles_n) * BM), n0 = (int)((r % tiles_n) * BN);
+        for (uint32_t kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t *st = smem + stage * C::STAGE_BYTES;
+          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          const int kx = (int)(kb * BK);
+          tma_load_2d(st, &args.tm[p][0], &full[stage], kx, m0);
+          tma_load_2d(st + C::A_BYTES, &args.tm[p][2], &full[stage], kx, n0);
+          if (SPLIT) {
+            tma_load_2d(st + C::A_BYTES + C::B_BYTES, &args.tm[p][1], &full[stage], kx, m0);
+            tma_load_2d(st + 2 * C::A_BYTES + C::B_BYTES, &args.tm[p][3], &full[stage], kx, n0);
+          }
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = idesc_bf16(BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+      for (uint32_t kb = 0; kb < kblocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t sb = sa + C::A_BYTES;
+          const uint32_t sal = sb + C::B_BYTES;
+          const uint32_t sbl = sal + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint32_t koff = (uint32_t)k * 32;
+            const uint64_t da = sw128_desc(sa + koff), db = sw128_desc(sb + koff);
+            tc_mma(d, da, db, idesc, (kb | (uint32_t)k) != 0);
+            if (SPLIT) {
+              tc_mma(d, da, sw128_desc(sbl + koff), idesc, 1u);
+              tc_mma(d, sw128_desc(sal + koff), db, idesc, 1u);
+            }
+          }
+          tc_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (lane == 0) tc_commit(&tfull[acc]);
+      __syncwarp();
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else {
+    // ------------------------------------------------ epilogue (warps 2..5)
+    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const uint32_t p = t / (tiles_m * tiles_n);
+      const uint32_t r = t % (tiles_m * tiles_n);
+      const uint32_t mt = r / tiles_n, nt = r % tiles_n;
+      const uint32_t m0 = mt * BM, n0 = nt * BN;
+      const uint32_t row = m0 + quad * 32 + lane;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN);
+      float run_max = -INFINITY, run_sum = 0.f, tgt = -INFINITY;
+      int64_t target = -1;
+      if (EPI == ZO2_EPI_CE && row < M) target = args.targets[p][row];
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(tbase + (uint32_t)c0, v);
+        const uint32_t col0 = n0 + (uint32_t)c0;
+        if (row < M && col0 < N) {
+          if (EPI == ZO2_EPI_CE) {
+            float cm = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < N) cm = fmaxf(cm, __uint_as_float(v[j]));
+            const float nm = fmaxf(run_max, cm);
+            float s = run_sum * expf(run_max - nm);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j < N) s += expf(__uint_as_float(v[j]) - nm);
+            run_sum = s;
+            run_max = nm;
+            if (target >= (int64_t)col0 && target < (int64_t)col0 + 32 && target < (int64_t)N) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if ((int64_t)col0 + j == target) tgt = __uint_as_float(v[j]);
+            }
+          } else {
+            const float *bias = args.bias[p];
+            float x[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              x[j] = __uint_as_float(v[j]);
+              if (bias && col0 + j < N) x[j] += bias[col0 + j];
+            }
+            const bool full_chunk = (col0 + 32 <= N) && (N % 4 == 0);
+            if (EPI == ZO2_EPI_STORE || EPI == ZO2_EPI_RESIDUAL) {
+              float *cp = (float *)args.c[p] + (uint64_t)row * N + col0;
+              if (full_chunk) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) {
+                  float4 o = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+                  if (EPI == ZO2_EPI_RESIDUAL) {
+                    const float4 h = *(const float4 *)(cp + j);
+                    o.x += h.x; o.y += h.y; o.z += h.z; o.w += h.w;
+                  }
+                  *(float4 *)(cp + j) = o;
+                }
+              } else {
+                for (int j = 0; j < 32 && col0 + j < N; ++j)
+                  cp[j] = (EPI == ZO2_EPI_RESIDUAL) ? cp[j] + x[j] : x[j];
+              }
+            } else {  // GELU -> bf16 operand planes
+              __nv_bfloat16 *hp = (__nv_bfloat16 *)args.c[p] + (uint64_t)row * N + col0;
+              __nv_bfloat16 *lp =
+                  SPLIT ? (__nv_bfloat16 *)args.c_lo[p] + (uint64_t)row * N + col0 : nullptr;
+              __align__(16) __nv_bfloat16 hv[32], lv[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const float g = gelu_erf(x[j]);
+                hv[j] = __float2bfloat16_rn(g);
+                lv[j] = __float2bfloat16_rn(g - __bfloat162float(hv[j]));
+              }
+              if (full_chunk && (N % 8 == 0)) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 8) {
+                  *(uint4 *)(hp + j) = *(const uint4 *)(hv + j);
+                  if (SPLIT) *(uint4 *)(lp + j) = *(const uint4 *)(lv + j);
+                }
+              } else {
+                for (int j = 0; j < 32 && col0 + j < N; ++j) {
+                  hp[j] = hv[j];
+                  if (SPLIT) lp[j] = lv[j];
+                }
+              }
+            }
+          }
+        }
+      }
+      if (EPI == ZO2_EPI_CE && row < M) {
+        float *o = args.ce_part[p] + ((uint64_t)row * tiles_n + nt) * 3;
+        o[0] = run_max;
+        o[1] = run_sum;
+        o[2] = tgt;
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"((uint32_t)C::TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::mutex g_mu;
+
+struct MapKey {
+  const void *p;
+  uint32_t rows, k, box_rows;
+  bool operator==(const MapKey &o) const {
+    return p == o.p && rows == o.rows && k == o.k && box_rows == o.box_rows;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey &k) const {
+    return std::hash<const void *>()(k.p) ^ ((size_t)k.rows * 1315423911u) ^
+           ((size_t)k.k << 20) ^ k.box_rows;
+  }
+};
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+int get_encoder() {
+  if (g_encode) return ZO2_OK;
+  cudaDriverEntryPointQueryResult q;
+  void *fn = nullptr;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+    return zo2_set_error(ZO2_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  return ZO2_OK;
+}
+
+int make_map(const void *ptr, uint32_t rows, uint32_t k, uint32_t box_rows, CUtensorMap *out) {
+  MapKey key{ptr, rows, k, box_rows};
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return ZO2_OK;
+    }
+  }
+  int rc = get_encoder();
+  if (rc) return rc;
+  cuuint64_t dims[2] = {k, rows};
+  cuuint64_t strides[1] = {(cuuint64_t)k * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char msg[160];
+    snprintf(msg, sizeof(msg), "cuTensorMapEncodeTiled failed (%d) rows=%u k=%u", (int)r, rows, k);
+    return zo2_set_error(ZO2_E_ARG, msg);
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_maps.size() > 4096) g_maps.clear();
+  g_maps[key] = *out;
+  return ZO2_OK;
+}
+
+int g_num_sms = 0;
+
+template <int BN, bool SPLIT, int EPI>
+int launch(const GemmArgs &a, cudaStream_t s) {
+  using C = Cfg<BN, SPLIT>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm<BN, SPLIT, EPI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return zo2_set_cuda_error(e);
+    attr_set = true;
+  }
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  const uint32_t tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN) * (uint32_t)a.batch;
+  const unsigned grid = tiles < (uint32_t)g_num_sms ? tiles : (unsigned)g_num_sms;
+  k_gemm<BN, SPLIT, EPI><<<grid, NUM_THREADS, C::SMEM, s>>>(a);
+  zo2_count_launch();
+  ZO2_CHECK_LAUNCH();
+  return ZO2_OK;
+}
+
+template <int BN, bool SPLIT>
+int dispatch_epi(const GemmArgs &a, int epi, cudaStream_t s) {
+  switch (epi) {
+    case ZO2_EPI_STORE: return launch<BN, SPLIT, ZO2_EPI_STORE>(a, s);
+    case ZO2_EPI_RESIDUAL: return launch<BN, SPLIT, ZO2_EPI_RESIDUAL>(a, s);
+    case ZO2_EPI_GELU: return launch<BN, SPLIT, ZO2_EPI_GELU>(a, s);
+    case ZO2_EPI_CE: return launch<BN, SPLIT, ZO2_EPI_CE>(a, s);
+    default: return zo2_set_error(ZO2_E_ARG, "zo2_gemm: unknown epilogue");
+  }
+}
+
+}  // namespace
+
+extern "C" int zo2_gemm_tile_n(int split) { return split ? 128 : 256; }
+
+extern "C" int zo2_gemm(const zo2_gemm_problem *probs, int batch, uint32_t M, uint32_t N,
+                        uint32_t K, int epi, void *cs) {
+  if (batch < 1 || batch > 2) return zo2_set_error(ZO2_E_ARG, "zo2_gemm: batch must be 1 or 2");
+  if (M == 0 || N == 0) return ZO2_OK;
+  if (K == 0 || K % 8 != 0) return zo2_set_error(ZO2_E_UNSUPPORTED, "zo2_gemm: K must be a positive multiple of 8");
+  const bool split = probs[0].a_lo != nullptr;
+  const int BN = split ? 128 : 256;
+  GemmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.batch = batch;
+  for (int p = 0; p < batch; ++p) {
+    const zo2_gemm_problem &q = probs[p];
+    if (!q.a_hi || !q.b_hi) return zo2_set_error(ZO2_E_ARG, "zo2_gemm: null operand");
+    if (split != (q.a_lo != nullptr) || split != (q.b_lo != nullptr))
+      return zo2_set_error(ZO2_E_ARG, "zo2_gemm: split planes must be given for A and B together");
+    int rc = make_map(q.a_hi, M, K, BM, &a.tm[p][0]);
+    if (!rc) rc = make_map(q.b_hi, N, K, (uint32_t)BN, &a.tm[p][2]);
+    if (!rc && split) rc = make_map(q.a_lo, M, K, BM, &a.tm[p][1]);
+    if (!rc && split) rc = make_map(q.b_lo, N, K, (uint32_t)BN, &a.tm[p][3]);
+    if (rc) return rc;
+    a.bias[p] = q.bias;
+    a.c[p] = q.c;
+    a.c_lo[p] = q.c_lo;
+    a.targets[p] = q.targets;
+    a.ce_part[p] = q.ce_part;
+    if (epi == ZO2_EPI_CE && (!q.targets || !q.ce_part))
+      return zo2_set_error(ZO2_E_ARG, "zo2_gemm: CE epilogue needs targets and ce_part");
+    if (epi != ZO2_EPI_CE && !q.c) return zo2_set_error(ZO2_E_ARG, "zo2_gemm: null output");
+    if (epi == ZO2_EPI_GELU && split && !q.c_lo)
+      return zo2_set_error(ZO2_E_ARG, "zo2_gemm: split GELU needs c_lo");
+  }
+  cudaStream_t s = (cudaStream_t)cs;
+  return split ? dispatch_epi<128, true>(a, epi, s) : dispatch_epi<256, false>(a, epi, s);
+}

@@ -1,0 +1,302 @@
+// zo2_layers.cu -- memory-bound forward kernels of the dual forward
+// (model.py:241-313): embedding gather with on-the-fly perturbation (K8),
+// LayerNorm (K4), causal attention (K5), cross-entropy reduction (K7 tail).
+#include "zo2_common.cuh"
+#include "zo2_rng.h"
+
+void zo2_count_launch(uint64_t n = 1);
+static inline cudaStream_t S(void *s) { return (cudaStream_t)s; }
+
+__device__ __forceinline__ float ax1(float w, double coef, double z) {
+  return __double2float_rn(__dadd_rn((double)w, __dmul_rn(coef, z)));
+}
+
+// ------------------------------------------------------------------ K8
+// One thread = 4 consecutive columns of one token.  tok and pos elements are
+// regenerated through the module's op sequence: update(lrs) then +eps, -2eps.
+__device__ __forceinline__ void embed_elem4(const float *table, uint64_t i, uint64_t base,
+                                            int upd, double ucoef, uint64_t lrs, double eps,
+                                            uint64_t rs, float wp[4], float wm[4]) {
+  float4 v = *(const float4 *)(table + i);
+  float w[4] = {v.x, v.y, v.z, v.w};
+  uint64_t r[4];
+  if (upd) {
+    zo2_raw_block(lrs, ZO2_PERTURB_STREAM, (base + i) >> 2, r);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w[j] = ax1(w[j], ucoef, zo2_ndtri(zo2_u53(r[j])));
+  }
+  zo2_raw_block(rs, ZO2_PERTURB_STREAM, (base + i) >> 2, r);
+  const double m2 = -2.0 * eps;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const double z = zo2_ndtri(zo2_u53(r[j]));
+    wp[j] = ax1(w[j], eps, z);
+    wm[j] = ax1(wp[j], m2, z);
+  }
+}
+
+__global__ void k_embed_dual(const int64_t *ids, uint64_t n_tok, uint32_t seq, uint32_t dim,
+                             uint32_t vocab, const float *table, uint64_t base, int upd,
+                             const double *d_g, double lr, uint64_t lrs, double eps,
+                             uint64_t rs, float *outp, float *outm) {
+  double ucoef = 0.0;
+  if (upd) {
+    const double g = *d_g;
+    if (g == 0.0) upd = 0;
+    else ucoef = -(lr * g);
+  }
+  const uint32_t q_per_tok = dim / 4;
+  const uint64_t total = n_tok * q_per_tok;
+  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < total;
+       q += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t t = q / q_per_tok;
+    const uint32_t c = (uint32_t)(q % q_per_tok) * 4;
+    const int64_t id = ids[t];
+    const uint32_t s = (uint32_t)(t % seq);
+    float tp[4], tm[4], pp[4], pm[4];
+    embed_elem4(table, (uint64_t)id * dim + c, base, upd, ucoef, lrs, eps, rs, tp, tm);
+    embed_elem4(table, (uint64_t)vocab * dim + (uint64_t)s * dim + c, base, upd, ucoef, lrs,
+                eps, rs, pp, pm);
+    *(float4 *)(outp + t * dim + c) =
+        make_float4(tp[0] + pp[0], tp[1] + pp[1], tp[2] + pp[2], tp[3] + pp[3]);
+    *(float4 *)(outm + t * dim + c) =
+        make_float4(tm[0] + pm[0], tm[1] + pm[1], tm[2] + pm[2], tm[3] + pm[3]);
+  }
+}
+
+extern "C" int zo2_embed_dual(const int64_t *ids, uint64_t n_tok, uint32_t seq, uint32_t dim,
+                              uint32_t vocab, uint32_t max_seq, const float *table,
+                              uint64_t base, int update, const double *d_g, double lr,
+                              uint64_t lrs_seed, double eps, uint64_t rs_seed, float *outp,
+                              float *outm, void *cs) {
+  if (n_tok == 0) return ZO2_OK;
+  if (dim % 4 != 0 || base % 4 != 0)
+    return zo2_set_error(ZO2_E_UNSUPPORTED, "zo2_embed_dual: dim and base must be multiples of 4");
+  if (seq > max_seq) return zo2_set_error(ZO2_E_ARG, "zo2_embed_dual: seq > max_seq");
+  if (update && !d_g) return zo2_set_error(ZO2_E_ARG, "zo2_embed_dual: update needs d_g");
+  const uint64_t total = n_tok * (dim / 4);
+  k_embed_dual<<<zo2_grid_for(total, 256, 148u * 16u), 256, 0, S(cs)>>>(
+      ids, n_tok, seq, dim, vocab, table, base, update, d_g, lr, lrs_seed, eps, rs_seed, outp,
+      outm);
+  zo2_count_launch();
+  ZO2_CHECK_LAUNCH();
+  return ZO2_OK;
+}
+
+// ------------------------------------------------------------------ K4
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int k = 0; k < NT / 32; ++k) t += sh[k];
+  return t;
+}
+
+// One CTA per row; the row stays in registers (dim <= 256 * 64).
+template <int NT, int MAXV>
+__global__ void __launch_bounds__(NT) k_layernorm(const float *x, uint32_t dim,
+                                                  const float *gamma, const float *beta,
+                                                  __nv_bfloat16 *out_hi, __nv_bfloat16 *out_lo) {
+  __shared__ double sh[NT / 32];
+  const uint64_t row = blockIdx.x;
+  const float *xr = x + row * dim;
+  float v[MAXV];
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < MAXV; ++k) {
+    const uint32_t c = threadIdx.x + k * NT;
+    v[k] = c < dim ? xr[c] : 0.f;
+    s += v[k];
+  }
+  const float mu = (float)(block_sum<NT>(s, sh) / dim);
+  double q = 0.0;
+#pragma unroll
+  for (int k = 0; k < MAXV; ++k) {
+    const uint32_t c = threadIdx.x + k * NT;
+    if (c < dim) {
+      const float d = v[k] - mu;
+      q += (double)d * d;
+    }
+  }
+  const float var = (float)(block_sum<NT>(q, sh) / dim);
+  const float inv = 1.0f / sqrtf(var + 1e-5f);
+#pragma unroll
+  for (int k = 0; k < MAXV; ++k) {
+    const uint32_t c = threadIdx.x + k * NT;
+    if (c < dim) {
+      const float y = (v[k] - mu) * inv * gamma[c] + beta[c];
+      const __nv_bfloat16 h = __float2bfloat16_rn(y);
+      out_hi[row * dim + c] = h;
+      if (out_lo) out_lo[row * dim + c] = __float2bfloat16_rn(y - __bfloat162float(h));
+    }
+  }
+}
+
+extern "C" int zo2_layernorm(const float *x, uint64_t rows, uint32_t dim, const float *gamma,
+                             const float *beta, void *out_hi, void *out_lo, void *cs) {
+  if (rows == 0) return ZO2_OK;
+  __nv_bfloat16 *hi = (__nv_bfloat16 *)out_hi, *lo = (__nv_bfloat16 *)out_lo;
+  if (dim <= 256 * 8)
+    k_layernorm<256, 8><<<(unsigned)rows, 256, 0, S(cs)>>>(x, dim, gamma, beta, hi, lo);
+  else if (dim <= 256 * 24)
+    k_layernorm<256, 24><<<(unsigned)rows, 256, 0, S(cs)>>>(x, dim, gamma, beta, hi, lo);
+  else if (dim <= 512 * 32)
+    k_layernorm<512, 32><<<(unsigned)rows, 512, 0, S(cs)>>>(x, dim, gamma, beta, hi, lo);
+  else
+    return zo2_set_error(ZO2_E_UNSUPPORTED, "zo2_layernorm: dim > 16384");
+  zo2_count_launch();
+  ZO2_CHECK_LAUNCH();
+  return ZO2_OK;
+}
+
+__global__ void k_to_operand(const float *x, uint64_t n, __nv_bfloat16 *hi,
+                             __nv_bfloat16 *lo) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const float v = x[i];
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    hi[i] = h;
+    if (lo) lo[i] = __float2bfloat16_rn(v - __bfloat162float(h));
+  }
+}
+
+extern "C" int zo2_to_operand(const float *x, uint64_t n, void *hi, void *lo, void *cs) {
+  if (n == 0) return ZO2_OK;
+  k_to_operand<<<zo2_grid_for(n, 256, 148u * 16u), 256, 0, S(cs)>>>(
+      x, n, (__nv_bfloat16 *)hi, (__nv_bfloat16 *)lo);
+  zo2_count_launch();
+  ZO2_CHECK_LAUNCH();
+  return ZO2_OK;
+}
+
+// ------------------------------------------------------------------ K5
+// SIMT flash attention (fp32): CTA = (query tile of 32, head, batch);
+// 8 lanes per query, each owning HD/8 dims of q and of the accumulator.
+template <int HD>
+__global__ void __launch_bounds__(256) k_attention(const float *qkv, uint32_t seq,
+                                                   uint32_t n_heads, __nv_bfloat16 *out_hi,
+                                                   __nv_bfloat16 *out_lo) {
+  constexpr int DPT = HD / 8;   // dims per thread
+  constexpr int KT = 32;        // keys per smem tile
+  __shared__ float ks[KT][HD + 4];
+  __shared__ float vs[KT][HD + 4];
+  const uint32_t dim = n_heads * HD;
+  const uint32_t ld = 3 * dim;
+  const uint32_t b = blockIdx.z, h = blockIdx.y;
+  const uint32_t q0 = blockIdx.x * 32;
+  const uint32_t qi = q0 + threadIdx.x / 8;
+  const uint32_t sub = threadIdx.x % 8;
+  const float scale = 1.0f / sqrtf((float)HD);
+  const float *base = qkv + (uint64_t)b * seq * ld;
+  float q[DPT], acc[DPT];
+  const bool valid = qi < seq;
+#pragma unroll
+  for (int j = 0; j < DPT; ++j) {
+    q[j] = valid ? base[(uint64_t)qi * ld + h * HD + sub * DPT + j] : 0.f;
+    acc[j] = 0.f;
+  }
+  float m = -INFINITY, l = 0.f;
+  const uint32_t kmax = min(seq, q0 + 32);  // causal: keys <= last query of tile
+  for (uint32_t k0 = 0; k0 < kmax; k0 += KT) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < KT * HD; e += 256) {
+      const int kr = e / HD, c = e % HD;
+      const uint32_t kk = k0 + kr;
+      ks[kr][c] = kk < seq ? base[(uint64_t)kk * ld + dim + h * HD + c] : 0.f;
+      vs[kr][c] = kk < seq ? base[(uint64_t)kk * ld + 2 * dim + h * HD + c] : 0.f;
+    }
+    __syncthreads();
+    const int kend = (int)min((uint32_t)KT, kmax - k0);
+    for (int kr = 0; kr < kend; ++kr) {
+      float sdot = 0.f;
+#pragma unroll
+      for (int j = 0; j < DPT; ++j) sdot += q[j] * ks[kr][sub * DPT + j];
+      sdot += __shfl_xor_sync(0xffffffffu, sdot, 1);
+      sdot += __shfl_xor_sync(0xffffffffu, sdot, 2);
+      sdot += __shfl_xor_sync(0xffffffffu, sdot, 4);
+      const uint32_t kk = k0 + kr;
+      if (valid && kk <= qi) {
+        const float sc = sdot * scale;
+        const float mn = fmaxf(m, sc);
+        const float corr = __expf(m - mn);
+        const float p = __expf(sc - mn);
+        l = l * corr + p;
+#pragma unroll
+        for (int j = 0; j < DPT; ++j) acc[j] = acc[j] * corr + p * vs[kr][sub * DPT + j];
+        m = mn;
+      }
+    }
+  }
+  if (valid) {
+    const float inv = 1.0f / l;
+    const uint64_t o = ((uint64_t)b * seq + qi) * dim + h * HD + sub * DPT;
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+      const float y = acc[j] * inv;
+      const __nv_bfloat16 hv = __float2bfloat16_rn(y);
+      out_hi[o + j] = hv;
+      if (out_lo) out_lo[o + j] = __float2bfloat16_rn(y - __bfloat162float(hv));
+    }
+  }
+}
+
+extern "C" int zo2_attention(const float *qkv, uint32_t batch, uint32_t seq, uint32_t n_heads,
+                             uint32_t head_dim, void *ctx_hi, void *ctx_lo, void *cs) {
+  if (batch == 0 || seq == 0) return ZO2_OK;
+  dim3 grid((seq + 31) / 32, n_heads, batch);
+  __nv_bfloat16 *hi = (__nv_bfloat16 *)ctx_hi, *lo = (__nv_bfloat16 *)ctx_lo;
+  switch (head_dim) {
+    case 8: k_attention<8><<<grid, 256, 0, S(cs)>>>(qkv, seq, n_heads, hi, lo); break;
+    case 16: k_attention<16><<<grid, 256, 0, S(cs)>>>(qkv, seq, n_heads, hi, lo); break;
+    case 32: k_attention<32><<<grid, 256, 0, S(cs)>>>(qkv, seq, n_heads, hi, lo); break;
+    case 64: k_attention<64><<<grid, 256, 0, S(cs)>>>(qkv, seq, n_heads, hi, lo); break;
+    case 128: k_attention<128><<<grid, 256, 0, S(cs)>>>(qkv, seq, n_heads, hi, lo); break;
+    default: return zo2_set_error(ZO2_E_UNSUPPORTED, "zo2_attention: head_dim not in {8,16,32,64,128}");
+  }
+  zo2_count_launch();
+  ZO2_CHECK_LAUNCH();
+  return ZO2_OK;
+}
+
+// ------------------------------------------------------------------ K7 tail
+// Combine per-(row, n-tile) partials {max, sum exp(x - max), target logit}
+// into sum over rows of (logsumexp - logit[target]) in f64.
+__global__ void k_ce_reduce(const float *part, uint32_t M, uint32_t n_tiles,
+                            uint64_t stride, double *sums) {
+  const int b = blockIdx.y;
+  const float *P = part + b * stride;
+  double acc = 0.0;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x) {
+    const float *pr = P + (uint64_t)r * n_tiles * 3;
+    double mx = -INFINITY, tgt = 0.0;
+    for (uint32_t t = 0; t < n_tiles; ++t) mx = fmax(mx, (double)pr[3 * t]);
+    double s = 0.0;
+    for (uint32_t t = 0; t < n_tiles; ++t) {
+      s += (double)pr[3 * t + 1] * exp((double)pr[3 * t] - mx);
+      const float tl = pr[3 * t + 2];
+      if (tl != -INFINITY) tgt = (double)tl;
+    }
+    acc += mx + log(s) - tgt;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&sums[b], acc);
+}
+
+extern "C" int zo2_ce_reduce(const float *part, uint32_t M, uint32_t n_tiles, int batch,
+                             uint64_t part_stride, double *d_sums, void *cs) {
+  if (M == 0) return ZO2_OK;
+  cudaError_t e = cudaMemsetAsync(d_sums, 0, sizeof(double) * batch, S(cs));
+  if (e != cudaSuccess) return zo2_set_cuda_error(e);
+  dim3 grid(zo2_grid_for(M, 256, 148), batch);
+  k_ce_reduce<<<grid, 256, 0, S(cs)>>>(part, M, n_tiles, part_stride, d_sums);
+  zo2_count_launch();
+  ZO2_CHECK_LAUNCH();
+  return ZO2_OK;
+}

@@ -1,0 +1,428 @@
+"""ZO2 and MeZO engines on B200 (drop-in for zo2lab zo2_engine.py / zo_ref.py).
+
+Zo2Engine keeps the reference's constructor, step/finalize/train contract and
+bookkeeping (RngStateManager FIFO, PendingGradient gate, DAG validation,
+zo2_engine.py:38-345); the arithmetic runs in the sm_100a library:
+
+  per module (zo2_engine.py:183-204 dual_forward), one compute-stream task:
+    K2  zo2_update_perturb: deferred update with lrs (gated on g != 0), then
+        +eps / -2eps / +eps with rs, emitting W+-eps z as GEMM operands and
+        leaving the restored weights in the arena (codec-encoded if active)
+    forward kernels for both signs (model.DualForward)
+  head: fused head GEMM + CE partials, CE reduce, K10 forms g on device; the
+  next step's K2 reads g from HBM, so no host round trip sits between steps'
+  kernels -- the host only reads (l+, l-, g) back for the returned value.
+Upload / offload run on their own streams (scheduler.enqueue_dag).
+"""
+from __future__ import annotations
+
+import math
+from collections import deque
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import NonFiniteLossError, SchedulingContractError, StateCorruptionError
+from .model import (EMBED_ID, HEAD_ID, DualForward, ModelSpec, module_order, module_size,
+                    rng_offsets)
+from .numerics import BATCH_STREAM, PERTURB_STREAM, RngState, derive_step_seed, raw_uint64
+from .runtime import ModelParams, OffloadRuntime
+from .scheduler import (CudaLanes, Lane, build_iteration_dag, ckey, enqueue_dag, okey, ukey,
+                        validate_timeline)
+
+
+@dataclass(frozen=True)
+class ZOConfig:
+    """zo_ref.py:29-42."""
+
+    eps: float
+    lr: float
+    steps: int
+    seed: int
+
+    def __post_init__(self):
+        if self.eps <= 0:
+            raise ValueError("eps must be > 0")
+        if self.lr <= 0:
+            raise ValueError("lr must be > 0")
+        if self.steps < 1:
+            raise ValueError("steps must be >= 1")
+
+
+def step_perturb_state(seed: int, step_index: int) -> RngState:
+    """zo_ref.py:45-46."""
+    return RngState(derive_step_seed(seed, step_index), PERTURB_STREAM, 0)
+
+
+def batch_for_step(seed: int, step_index: int, n_samples: int, batch_size: int) -> np.ndarray:
+    """zo_ref.py:49-56: batch indices from the BATCH stream."""
+    if n_samples < 1:
+        raise ValueError("cannot sample from an empty dataset")
+    raw, _ = raw_uint64(RngState(derive_step_seed(seed, step_index), BATCH_STREAM, 0),
+                        batch_size)
+    return (raw % np.uint64(n_samples)).astype(np.int64)
+
+
+@dataclass
+class PendingGradient:
+    """zo2_engine.py:38-51: one scalar, valid iff g != 0."""
+
+    g: float = 0.0
+    valid: bool = False
+
+    def set(self, g: float) -> None:
+        self.g = float(g)
+        self.valid = g != 0.0
+
+    def clear(self) -> None:
+        self.g = 0.0
+        self.valid = False
+
+
+@dataclass
+class _RsbEntry:
+    step: int
+    module: str
+    state: RngState
+
+
+class RngStateManager:
+    """zo2_engine.py:61-110 (rsb FIFO + lrs_map); misalignment is fatal."""
+
+    def __init__(self, seed: int):
+        self.seed = seed
+        self.rsb: deque[_RsbEntry] = deque()
+        self.lrs_map: dict[str, RngState] = {}
+        self.storage: dict[int, RngState] = {}
+        self.current_seed: int | None = None
+
+    def begin_iteration(self, step_seed: int) -> None:
+        self.current_seed = step_seed
+        self.set_state(step_seed, RngState(step_seed, PERTURB_STREAM, 0))
+
+    def set_state(self, seed: int, state: RngState) -> None:
+        self.storage[seed] = state
+
+    def get_state(self, seed: int | None = None) -> RngState:
+        return self.storage[self.current_seed if seed is None else seed]
+
+    def push_rs(self, step: int, module: str, state: RngState) -> None:
+        self.rsb.append(_RsbEntry(step, module, state))
+        self.lrs_map[module] = state
+
+    def _pop(self, module: str) -> RngState:
+        e = self.rsb.popleft()
+        if e.module != module:
+            raise StateCorruptionError(f"rsb misaligned: expected {module}, found {e.module} "
+                                       f"from step {e.step}")
+        return e.state
+
+    def pop_backlog(self, module: str, current_step: int) -> RngState | None:
+        if self.rsb and self.rsb[0].step < current_step:
+            return self._pop(module)
+        return None
+
+    def pop_current(self, module: str, current_step: int) -> RngState:
+        if not self.rsb or self.rsb[0].step != current_step:
+            raise StateCorruptionError(f"no state recorded for {module} in step {current_step}")
+        return self._pop(module)
+
+
+@dataclass
+class ModuleHandle:
+    module: str
+    size: int
+    transferable: bool
+
+
+class TransformerWorkload:
+    """Adapter the engines drive (model.py:335-393 surface): module sequence and
+    shapes; the forward itself runs in DualForward on the device."""
+
+    def __init__(self, params: ModelParams, arith: str = "f32"):
+        self.params = params
+        self.spec: ModelSpec = params.spec
+        self.arith = arith
+
+    def modules(self) -> list[ModuleHandle]:
+        return [ModuleHandle(m, module_size(self.spec, m), m not in (EMBED_ID, HEAD_ID))
+                for m in module_order(self.spec)]
+
+    @property
+    def tied_stash_bytes(self) -> int:
+        return 0  # the tied head reads the embedding's W+- operands directly
+
+    def activation_bytes(self, module: str, batch_size: int) -> int:
+        width = self.spec.vocab if module == HEAD_ID else self.spec.dim
+        return batch_size * self.spec.seq_len * width * 4
+
+
+class _DeviceStep:
+    """Shared device state of both engines: dual forward, scalars, pinned I/O."""
+
+    def __init__(self, spec: ModelSpec, arith: str, device):
+        self.spec, self.arith, self.device = spec, arith, torch.device(device)
+        self.fwd: DualForward | None = None
+        self.d_out = torch.zeros(3, dtype=torch.float64, device=self.device)  # l+, l-, g
+        self.d_flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.h_out = torch.zeros(4, dtype=torch.float64, pin_memory=True)
+        self.h_tok = None
+        self.offsets = rng_offsets(spec)
+
+    def ensure(self, batch_size: int) -> DualForward:
+        if self.fwd is None or self.fwd.B != batch_size:
+            self.fwd = None
+            torch.cuda.empty_cache()
+            self.fwd = DualForward(self.spec, batch_size, self.arith, self.device)
+            T = self.fwd.T
+            self.h_tok = torch.empty(2, T, dtype=torch.int64, pin_memory=True)
+        return self.fwd
+
+    def stage_batch(self, batch, stream: torch.cuda.Stream) -> tuple[int, int]:
+        tokens, targets = (np.asarray(x) for x in batch)
+        if tokens.ndim != 2 or tokens.shape != targets.shape:
+            raise ValueError(f"tokens {tokens.shape} / targets {targets.shape} must be (B, S)")
+        if tokens.shape[1] > self.spec.seq_len:
+            raise ValueError(f"tokens shape {tokens.shape} invalid for seq_len {self.spec.seq_len}")
+        if tokens.shape[1] != self.spec.seq_len:
+            raise ValueError("the B200 forward requires full-length sequences (S == seq_len)")
+        if tokens.min() < 0 or tokens.max() >= self.spec.vocab:
+            raise ValueError("token id out of range")
+        fwd = self.ensure(tokens.shape[0])
+        self.h_tok[0].numpy()[:] = tokens.reshape(-1)
+        self.h_tok[1].numpy()[:] = targets.reshape(-1)
+        with torch.cuda.stream(stream):
+            fwd.ids.copy_(self.h_tok[0], non_blocking=True)
+            fwd.targets.copy_(self.h_tok[1], non_blocking=True)
+        return tokens.shape[0], tokens.shape[1]
+
+    def read_out(self, stream: torch.cuda.Stream) -> None:
+        with torch.cuda.stream(stream):
+            self.h_out[:3].copy_(self.d_out, non_blocking=True)
+            self.h_out[3:4].copy_(self.d_flag.to(torch.float64), non_blocking=True)
+
+
+class Zo2Engine:
+    """Block-offloaded dual-forward optimizer on B200 (zo2_engine.py:113-345)."""
+
+    def __init__(self, workload: TransformerWorkload, cfg: ZOConfig, runtime: OffloadRuntime,
+                 *, overlap: bool = True, backend: str = "cuda", update_mode: str = "deferred",
+                 cost=None, trace=None, validate: bool = True):
+        if update_mode not in ("deferred", "naive"):
+            raise ValueError(f"unknown update_mode {update_mode!r}")
+        if overlap and runtime.k_slots < 3:
+            raise ValueError("overlap requires at least 3 arena slots")
+        if backend != "cuda":
+            raise ValueError("this engine runs on the 'cuda' backend only")
+        self.workload, self.cfg, self.runtime = workload, cfg, runtime
+        self.overlap, self.backend, self.update_mode = overlap, backend, update_mode
+        self.cost, self.trace, self.validate = cost, trace, validate
+        self.mgr = RngStateManager(cfg.seed)
+        self.pending = PendingGradient()
+        self.losses: list[float] = []
+        self.losses_minus: list[float] = []
+        self.gs: list[float] = []
+        self.timelines = []
+        self._handles = {h.module: h for h in workload.modules()}
+        self._order = [h.module for h in workload.modules()]
+        self._blocks = [m for m in self._order if self._handles[m].transferable]
+        self.lanes = CudaLanes(runtime.device)
+        self.dev = _DeviceStep(workload.spec, workload.arith, runtime.device)
+        self._lrs_seed_of: dict[str, int] = {}
+        self._pool_booked = False
+
+    # -- bookkeeping of one module visit (zo2_engine.py:187-203) -------------
+    def _visit(self, module: str, step: int) -> tuple[RngState, RngState | None, bool]:
+        rs = self.mgr.get_state()
+        if rs.counter != self.dev.offsets[module]:
+            raise StateCorruptionError(f"rs counter {rs.counter} != bucket offset of {module}")
+        lrs = self.mgr.pop_backlog(module, step)
+        update = self.pending.valid
+        if update and lrs is None:
+            raise StateCorruptionError(f"pending update for {module} but no saved state (lrs)")
+        self.mgr.push_rs(step, module, rs)
+        size = self._handles[module].size
+        self._emit("update", module, -(self.cfg.lr * self.pending.g), lrs) if update and size else None
+        self._emit("perturb", module, self.cfg.eps, rs) if size else None
+        self.mgr.set_state(rs.seed, rs.advanced(size))
+        return rs, lrs, update
+
+    def _emit(self, op: str, module: str, coef: float, state: RngState | None) -> None:
+        if self.trace is not None and state is not None:
+            self.trace({"op": op, "module": module, "coef": coef,
+                        "state": (state.seed, state.stream, state.counter)})
+
+    def _k2(self, buf: torch.Tensor, fmt_code: int, module: str, update: int, lrs_seed: int,
+            perturb: bool, rs_seed: int, descs, stream) -> None:
+        n = self._handles[module].size
+        if n == 0:
+            return
+        _lib.call("zo2_update_perturb", buf.data_ptr(), fmt_code, n, self.dev.offsets[module],
+                  int(update), self.dev.d_out[2:].data_ptr(), self.cfg.lr, lrs_seed,
+                  int(perturb), self.cfg.eps, rs_seed, descs, len(descs),
+                  self.runtime.d_conv.data_ptr(), stream.cuda_stream)
+
+    # -- per-module compute tasks -------------------------------------------
+    def _compute(self, module: str, step: int, seq: int, stream: torch.cuda.Stream) -> None:
+        fwd = self.dev.fwd
+        naive = self.update_mode == "naive"
+        if naive:
+            rs = self.mgr.get_state()
+            self.mgr.push_rs(step, module, rs)
+            self.mgr.set_state(rs.seed, rs.advanced(self._handles[module].size))
+            lrs, update = None, False
+        else:
+            rs, lrs, update = self._visit(module, step)
+        lrs_seed = lrs.seed if lrs is not None else 0
+        s = stream.cuda_stream
+        if module == EMBED_ID:
+            table = self.runtime.persistent[EMBED_ID]
+            fwd.embed_forward(table, self.dev.offsets[EMBED_ID], update,
+                              self.dev.d_out[2:], self.cfg.lr, lrs_seed, self.cfg.eps, rs.seed,
+                              seq, s)
+            self._k2(table, _lib.F32, module, update, lrs_seed, True, rs.seed,
+                     fwd.embed_descs(), stream)
+        elif module == HEAD_ID:
+            self._k2(self.runtime.persistent[HEAD_ID], _lib.F32, module, update, lrs_seed, True,
+                     rs.seed, fwd.head_descs(), stream)
+            fwd.head_forward(s)
+            _lib.call("zo2_form_g", fwd.d_sums.data_ptr(), float(fwd.T), self.cfg.eps,
+                      self.dev.d_out.data_ptr(), self.dev.d_flag.data_ptr(), s)
+        else:
+            slot = self.runtime.slot_for(self._blocks.index(module))
+            self._k2(self.runtime.slot_bucket(slot), self.runtime.wire_fmt.code, module, update,
+                     lrs_seed, True, rs.seed, fwd.block_descs(), stream)
+            fwd.block_forward(s)
+
+    def _naive_update(self, module: str, step: int, stream: torch.cuda.Stream) -> None:
+        """zo2_engine.py:251-260: update after g with the same-step state (no gate)."""
+        rs = self.mgr.pop_current(module, step)
+        if self._handles[module].size == 0:
+            return
+        self._emit("update", module, float("nan"), rs)
+        if module in (EMBED_ID, HEAD_ID):
+            buf, code = self.runtime.persistent[module], _lib.F32
+        else:
+            buf = self.runtime.slot_bucket(self.runtime.slot_for(self._blocks.index(module)))
+            code = self.runtime.wire_fmt.code
+        descs = self._update_descs(module)
+        self._k2(buf, code, module, 2, rs.seed, False, 0, descs, stream)
+
+    def _update_descs(self, module: str):
+        from .model import module_layout, segments
+        segs = segments(module_layout(self.workload.spec, module))
+        arr = (_lib.SegmentDesc * len(segs))()
+        for k, sg in enumerate(segs):
+            arr[k].offset = sg.offset
+            arr[k].rows = 1 if len(sg.shape) == 1 else sg.shape[0]
+            arr[k].cols = sg.shape[-1]
+            arr[k].out_kind = _lib.OUT_NONE
+        return arr
+
+    def _book_pool(self, fwd: DualForward) -> None:
+        if self._pool_booked:
+            return
+        for cat, nb in fwd.nbytes().items():
+            self.runtime.pool.alloc(cat, nb)
+        self._pool_booked = True
+
+    # -- one iteration (zo2_engine.py:264-316) --------------------------------
+    def step(self, batch, step_index: int) -> float:
+        cfg, rt = self.cfg, self.runtime
+        rt.current_step = step_index
+        self.mgr.begin_iteration(derive_step_seed(cfg.seed, step_index))
+        comp = self.lanes[Lane.COMPUTE]
+        _, seq = self.dev.stage_batch(batch, comp)
+        self._book_pool(self.dev.fwd)
+        naive = self.update_mode == "naive"
+        wire = {b: rt.block_nbytes for b in self._blocks}
+        dag = build_iteration_dag(self._blocks, k_slots=rt.k_slots, overlap=self.overlap,
+                                  naive_update=naive, wire_bytes=wire,
+                                  embed_id=self._order[0], head_id=self._order[-1])
+        fns = {ckey(m): (lambda st, m=m: self._compute(m, step_index, seq, st))
+               for m in self._order}
+        for i, b in enumerate(self._blocks):
+            slot = rt.slot_for(i)
+            fns[ukey(b)] = lambda st, b=b, slot=slot: rt.upload(b, slot, step_index, st, ukey(b))
+            fns[okey(b)] = lambda st, b=b, slot=slot: rt.offload(b, slot, step_index, st, okey(b))
+            if naive:
+                fns[ukey(b, 2)] = (lambda st, b=b, slot=slot:
+                                   rt.upload(b, slot, step_index, st, ukey(b, 2)))
+                fns[okey(b, 2)] = (lambda st, b=b, slot=slot:
+                                   rt.offload(b, slot, step_index, st, okey(b, 2)))
+        if naive:
+            for m in self._order:
+                fns[ckey(m, 2)] = lambda st, m=m: self._naive_update(m, step_index, st)
+        enq = enqueue_dag(dag, self.lanes, fns)
+        self.dev.read_out(comp)
+        self.lanes.synchronize()
+        timeline = enq.timeline()
+        rt.commit_records(timeline)
+        lp, lm, g, flag = (float(x) for x in self.dev.h_out.tolist())
+        if flag != 0.0 or not (math.isfinite(lp) and math.isfinite(lm)):
+            raise NonFiniteLossError(f"step {step_index}: l+={lp}, l-={lm}")
+        if self.validate:
+            bad = validate_timeline(timeline, dag, tol=2e-6)
+            if bad:
+                raise SchedulingContractError("; ".join(str(v) for v in bad[:5]))
+        self.timelines.append((step_index, timeline))
+        if naive:
+            self.pending.clear()
+        else:
+            self.pending.set(g)
+        expected = 0 if naive else len(self._order)
+        if len(self.mgr.rsb) != expected:
+            raise StateCorruptionError(f"rsb holds {len(self.mgr.rsb)} entries, "
+                                       f"expected {expected}")
+        self.losses.append(lp)
+        self.losses_minus.append(lm)
+        self.gs.append(g)
+        return g
+
+    def force_pending(self, g: float) -> None:
+        """Parity hook: replace the pending projected gradient with an
+        externally supplied value (e.g. the reference's g for this step), so the
+        next step's deferred update -- and finalize -- use exactly it."""
+        self.pending.set(g)
+        self.dev.d_out[2].fill_(float(g))
+        torch.cuda.synchronize(self.runtime.device)
+
+    def finalize(self) -> ModelParams:
+        """Drain the last pending update (zo2_engine.py:318-336); idempotent."""
+        rt = self.runtime
+        if self.pending.valid:
+            comp = self.lanes[Lane.COMPUTE]
+            for module in self._order:
+                h = self._handles[module]
+                if h.size == 0:
+                    continue
+                lrs = self.mgr.lrs_map.get(module)
+                if lrs is None:
+                    raise StateCorruptionError(f"finalize: no lrs for {module}")
+                descs = self._update_descs(module)
+                if h.transferable:
+                    slot = 0
+                    with torch.cuda.stream(comp):
+                        rt.slots[slot].copy_(rt.host[module], non_blocking=True)
+                    self._k2(rt.slots[slot], rt.wire_fmt.code, module, 1, lrs.seed, False, 0,
+                             descs, comp)
+                    with torch.cuda.stream(comp):
+                        rt.host[module].copy_(rt.slots[slot], non_blocking=True)
+                    comp.synchronize()
+                else:
+                    self._k2(rt.persistent[module], _lib.F32, module, 1, lrs.seed, False, 0,
+                             descs, comp)
+            comp.synchronize()
+        self.pending.clear()
+        self.mgr.rsb.clear()
+        return rt.export_params()
+
+    def train(self, dataset, steps: int | None = None) -> list[float]:
+        steps = self.cfg.steps if steps is None else steps
+        for j in range(steps):
+            idx = batch_for_step(self.cfg.seed, j, dataset.n_samples, dataset.batch_size)
+            self.step(dataset.batch(idx), j)
+        self.finalize()
+        return self.losses

@@ -1,0 +1,311 @@
+"""Two-tier memory for the B200 offload step (replaces zo2lab runtime.py).
+
+Host tier: one pinned (cudaHostAlloc) master per transformer block, in the
+wire format: the arithmetic format (f32) or, with a codec, the low-bit
+encoding (runtime.py:145-199 HostBlockStore; "the full-precision
+copy exists only on the device").  Device tier: K reusable arenas in the same
+wire format plus the resident embedding and LM head in f32 (runtime.py:228-247).
+Upload / offload are cudaMemcpyAsync on the upload / offload streams; the
+codec is applied on device inside the fused update/perturb kernel (K2), so
+the wire carries exactly `wire bytes` and nothing is staged on the host.
+
+Accounting (DevicePool, runtime.py:94-142) books every real device allocation
+by category and enforces device_capacity_bytes (CapacityError).
+"""
+from __future__ import annotations
+
+import hashlib
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import CapacityError, SchedulingContractError
+from .model import (EMBED_ID, HEAD_ID, ModelSpec, block_id, init_module_, module_order,
+                    module_size)
+from .numerics import CODEC_FORMATS, ConversionSummary, ElemFormat, RngState
+
+_TORCH_STORAGE = {ElemFormat.F64: torch.float64, ElemFormat.F32: torch.float32,
+                  ElemFormat.F16: torch.int16, ElemFormat.BF16: torch.int16,
+                  ElemFormat.F8E4M3: torch.uint8}
+
+
+@dataclass
+class TransferRecord:
+    module: str
+    direction: str
+    bytes_wire: int
+    fmt_wire: ElemFormat
+    t_start: float
+    t_end: float
+    step: int = 0
+
+    def to_json(self) -> dict:
+        return {"module": self.module, "direction": self.direction,
+                "bytes_wire": self.bytes_wire, "fmt_wire": self.fmt_wire.tag,
+                "t_start": self.t_start, "t_end": self.t_end, "step": self.step}
+
+
+class TransferLog:
+    """Append-only transfer log (runtime.py:44-69)."""
+
+    def __init__(self):
+        self._records: list[TransferRecord] = []
+        self._lock = threading.Lock()
+
+    def append(self, rec: TransferRecord) -> None:
+        with self._lock:
+            self._records.append(rec)
+
+    def records(self) -> list[TransferRecord]:
+        with self._lock:
+            return list(self._records)
+
+    def counts(self) -> dict[tuple[str, str], int]:
+        out: dict[tuple[str, str], int] = {}
+        for r in self.records():
+            out[(r.module, r.direction)] = out.get((r.module, r.direction), 0) + 1
+        return out
+
+    def wire_bytes(self, direction: str | None = None) -> int:
+        return sum(r.bytes_wire for r in self.records()
+                   if direction is None or r.direction == direction)
+
+
+class DevicePool:
+    """Byte accountant with capacity enforcement (runtime.py:94-142)."""
+
+    def __init__(self, capacity_bytes: float = float("inf")):
+        self.capacity = capacity_bytes
+        self._used: dict[str, int] = {}
+        self.peak_used = 0
+        self._lock = threading.Lock()
+
+    def alloc(self, category: str, nbytes: int) -> None:
+        if nbytes < 0:
+            raise ValueError("allocation size must be >= 0")
+        with self._lock:
+            used = sum(self._used.values()) + nbytes
+            if used > self.capacity:
+                raise CapacityError(f"alloc {nbytes} B for {category}: {used} B exceeds "
+                                    f"capacity {self.capacity} B")
+            self._used[category] = self._used.get(category, 0) + nbytes
+            self.peak_used = max(self.peak_used, used)
+
+    def free(self, category: str, nbytes: int) -> None:
+        with self._lock:
+            have = self._used.get(category, 0)
+            if nbytes > have:
+                raise ValueError(f"freeing {nbytes} B from {category}, only {have} B live")
+            self._used[category] = have - nbytes
+
+    @property
+    def used(self) -> int:
+        with self._lock:
+            return sum(self._used.values())
+
+    def breakdown(self) -> dict[str, int]:
+        with self._lock:
+            return dict(self._used)
+
+
+class ModelParams:
+    """Parameter buckets of one model: embedding and head resident on device
+    (f32), blocks as pinned host f32 masters (model.py:158-181 layout)."""
+
+    def __init__(self, spec: ModelSpec, embedding: torch.Tensor, blocks: list[torch.Tensor],
+                 lm_head: torch.Tensor, fmt: ElemFormat = ElemFormat.F32):
+        self.spec, self.embedding, self.blocks, self.lm_head, self.fmt = (
+            spec, embedding, blocks, lm_head, fmt)
+
+    def buckets(self) -> list[tuple[str, torch.Tensor]]:
+        return ([(EMBED_ID, self.embedding)] +
+                [(block_id(i), b) for i, b in enumerate(self.blocks)] + [(HEAD_ID, self.lm_head)])
+
+    def bucket(self, module: str) -> torch.Tensor:
+        if module == EMBED_ID:
+            return self.embedding
+        if module == HEAD_ID:
+            return self.lm_head
+        return self.blocks[int(module.split(".", 1)[1])]
+
+    def total_params(self) -> int:
+        return sum(b.numel() for _, b in self.buckets())
+
+    def to_numpy(self) -> dict[str, np.ndarray]:
+        return {m: b.detach().cpu().numpy().copy() for m, b in self.buckets()}
+
+    @classmethod
+    def from_numpy(cls, spec: ModelSpec, flats: dict[str, np.ndarray], device="cuda",
+                   pin: bool = True) -> "ModelParams":
+        """Adopt reference buckets (e.g. zo2lab init_params(...).buckets())."""
+        def dev(a):
+            return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(device)
+        blocks = []
+        for i in range(spec.n_blocks):
+            t = torch.from_numpy(np.ascontiguousarray(flats[block_id(i)], dtype=np.float32))
+            blocks.append(t.pin_memory() if pin else t.clone())
+        head = flats.get(HEAD_ID, np.zeros(0, np.float32))
+        return cls(spec, dev(flats[EMBED_ID]), blocks, dev(head))
+
+
+def init_params(spec: ModelSpec, state: RngState, fmt: ElemFormat = ElemFormat.F32,
+                device="cuda", pin: bool = True) -> ModelParams:
+    """model.py:198-224 on device: bit-identical buckets, blocks then moved to
+    pinned host memory (the offload tier)."""
+    if fmt is not ElemFormat.F32:
+        raise ValueError("the B200 engine keeps parameters in f32 (arith f32 / bf16)")
+    seed = state.seed
+    emb = torch.empty(module_size(spec, EMBED_ID), dtype=torch.float32, device=device)
+    init_module_(spec, EMBED_ID, seed, emb)
+    head = torch.empty(module_size(spec, HEAD_ID), dtype=torch.float32, device=device)
+    if head.numel():
+        init_module_(spec, HEAD_ID, seed, head)
+    blocks = []
+    scratch = torch.empty(module_size(spec, block_id(0)), dtype=torch.float32, device=device)
+    for i in range(spec.n_blocks):
+        init_module_(spec, block_id(i), seed, scratch)
+        host = torch.empty(scratch.numel(), dtype=torch.float32, pin_memory=pin)
+        host.copy_(scratch)
+        blocks.append(host)
+    torch.cuda.synchronize()
+    return ModelParams(spec, emb, blocks, head, fmt)
+
+
+def params_digest(params) -> str:
+    """SHA-256 over canonical bucket bytes (metrics.py:20-27); equal digests
+    mean identical models.  Accepts our ModelParams or {module: ndarray}."""
+    h = hashlib.sha256()
+    items = (params.to_numpy().items() if isinstance(params, ModelParams)
+             else params.items())
+    for module, flat in items:
+        flat = np.asarray(flat)
+        tag = "f64" if flat.dtype == np.float64 else "f32"
+        h.update(module.encode())
+        h.update(tag.encode())
+        h.update(flat.tobytes())
+    return h.hexdigest()
+
+
+class OffloadRuntime:
+    """Pinned host masters + K device arenas + transfer log + pool, for one run
+    (runtime.py:202-304 surface)."""
+
+    def __init__(self, params: ModelParams, *, k_slots: int = 3, codec: str | None = None,
+                 capacity_bytes: float = float("inf"), device="cuda"):
+        self.params = params
+        self.spec = params.spec
+        self.k_slots = int(k_slots)
+        self.codec = CODEC_FORMATS[codec] if codec not in (None, "none") else None
+        self.wire_fmt = self.codec or params.fmt
+        self.device = torch.device(device)
+        self.pool = DevicePool(capacity_bytes)
+        self.log = TransferLog()
+        self.conversion = ConversionSummary()
+        self.current_step = 0
+        self._block_ids = [block_id(i) for i in range(self.spec.n_blocks)]
+        self.block_size = module_size(self.spec, block_id(0)) if self._block_ids else 0
+        self.d_conv = torch.zeros(2, dtype=torch.int64, device=self.device)
+        sdt = _TORCH_STORAGE[self.wire_fmt]
+        # host stores (HostBlockStore): alias the f32 masters, or encode them
+        self.host: dict[str, torch.Tensor] = {}
+        if self.codec is None:
+            for i, b in enumerate(self._block_ids):
+                self.host[b] = params.blocks[i]
+        else:
+            scratch = torch.empty(self.block_size, dtype=torch.float32, device=self.device)
+            enc = torch.empty(self.block_size, dtype=sdt, device=self.device)
+            s = torch.cuda.current_stream().cuda_stream
+            for i, b in enumerate(self._block_ids):
+                scratch.copy_(params.blocks[i])
+                _lib.call("zo2_encode", scratch.data_ptr(), enc.data_ptr(), self.codec.code,
+                          self.block_size, self.d_conv.data_ptr(), s)
+                host = torch.empty(self.block_size, dtype=sdt, pin_memory=True)
+                host.copy_(enc)
+                self.host[b] = host
+            del scratch, enc
+            torch.cuda.synchronize()
+        # persistent residents: embedding and LM head (f32, never evicted)
+        self.persistent = {EMBED_ID: params.embedding, HEAD_ID: params.lm_head}
+        for t in self.persistent.values():
+            self.pool.alloc("persistent_params", t.numel() * 4)
+        # K arenas in wire format
+        self.pool.alloc("block_arenas", self.k_slots * self.block_nbytes)
+        self.slots = [torch.empty(self.block_size, dtype=sdt, device=self.device)
+                      for _ in range(self.k_slots)]
+        self._slot_owner: list[str | None] = [None] * self.k_slots
+        self._pending_records: list[tuple[TransferRecord, str]] = []
+
+    @property
+    def block_nbytes(self) -> int:
+        return self.block_size * self.wire_fmt.bytes_per_elem
+
+    def slot_for(self, block_index: int) -> int:
+        return block_index % self.k_slots
+
+    def slot_bucket(self, slot: int) -> torch.Tensor:
+        return self.slots[slot]
+
+    def host_param_bytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in self.host.values())
+
+    # -- transfers (enqueue only; times are filled from CUDA events) --------
+    def upload(self, module: str, slot: int, step: int, stream: torch.cuda.Stream,
+               key: str | None = None) -> None:
+        if self._slot_owner[slot] is not None:
+            raise SchedulingContractError(
+                f"upload of {module} into slot {slot} still owned by "
+                f"{self._slot_owner[slot]} (scheduler bug)")
+        with torch.cuda.stream(stream):
+            self.slots[slot].copy_(self.host[module], non_blocking=True)
+        self._slot_owner[slot] = module
+        rec = TransferRecord(module, "upload", self.block_nbytes, self.wire_fmt, 0.0, 0.0, step)
+        self._pending_records.append((rec, key or f"U:{module}"))
+
+    def offload(self, module: str, slot: int, step: int, stream: torch.cuda.Stream,
+                key: str | None = None) -> None:
+        if self._slot_owner[slot] != module:
+            raise SchedulingContractError(
+                f"offload of {module} from slot {slot} owned by {self._slot_owner[slot]} "
+                f"(scheduler bug)")
+        with torch.cuda.stream(stream):
+            self.host[module].copy_(self.slots[slot], non_blocking=True)
+        self._slot_owner[slot] = None
+        rec = TransferRecord(module, "offload", self.block_nbytes, self.wire_fmt, 0.0, 0.0, step)
+        self._pending_records.append((rec, key or f"O:{module}"))
+
+    def commit_records(self, timeline) -> None:
+        """Stamp the step's transfer records with device times and log them."""
+        ev = timeline.by_key()
+        for rec, key in self._pending_records:
+            if key in ev:
+                rec.t_start, rec.t_end = ev[key].t_start, ev[key].t_end
+            self.log.append(rec)
+        self._pending_records.clear()
+        nan, sat = (int(x) for x in self.d_conv.tolist())
+        self.conversion.nan_count, self.conversion.saturated_count = nan, sat
+
+    def export_params(self) -> ModelParams:
+        """Make the model's own buckets reflect the host masters (runtime.py:290-294)."""
+        if self.codec is not None:
+            scratch = torch.empty(self.block_size, dtype=torch.float32, device=self.device)
+            enc = torch.empty(self.block_size, dtype=self.slots[0].dtype, device=self.device)
+            s = torch.cuda.current_stream().cuda_stream
+            for i, b in enumerate(self._block_ids):
+                enc.copy_(self.host[b])
+                _lib.call("zo2_decode", enc.data_ptr(), scratch.data_ptr(), self.codec.code,
+                          self.block_size, s)
+                self.params.blocks[i].copy_(scratch)
+            torch.cuda.synchronize()
+        return self.params
+
+    def memory_report(self) -> dict:
+        return {"device_peak_bytes": self.pool.peak_used,
+                "device_used_bytes": self.pool.used,
+                "host_param_bytes": self.host_param_bytes(),
+                "breakdown": self.pool.breakdown(),
+                "conversion": {"nan_count": self.conversion.nan_count,
+                               "saturated_count": self.conversion.saturated_count},
+                "torch_max_allocated": int(torch.cuda.max_memory_allocated(self.device))}

@@ -1,0 +1,381 @@
+"""Parity of the sm_100a kernels against the CPU oracle / torch fp32 references.
+
+Integer/bit work (Philox, z, perturb/update arithmetic, codecs) must be
+bit-exact with the oracle (which is pinned to the reference by
+tests/golden).  The GEMM / LayerNorm / attention / CE kernels are floating
+point: tolerances are written per test.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def L():
+    from paper_2503_12668_b200 import _lib
+    return _lib
+
+
+def stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+# ------------------------------------------------------------------ K1
+def test_z_fill_bit_exact(cuda, oracle, golden):
+    for c in golden("rng.json")["gauss"]:
+        out = torch.empty(c["n"], dtype=torch.float64, device=cuda)
+        L().call("zo2_z_fill", out.data_ptr(), c["n"], c["seed"], c["stream"], c["counter"],
+                 stream())
+        assert [int(x) for x in out.cpu().numpy().view(np.uint64)] == c["bits"]
+    b = golden("rng.json")["bulk"]
+    out = torch.empty(b["n"], dtype=torch.float64, device=cuda)
+    L().call("zo2_z_fill", out.data_ptr(), b["n"], b["seed"], b["stream"], b["counter"], stream())
+    z = out.cpu().numpy()
+    assert int(np.sum(z.view(np.uint64), dtype=np.uint64)) == b["sum_bits_mod64"]
+
+
+@pytest.mark.parametrize("seed,counter,n", [(1, 0, 4_000_000), (2**63 + 11, 10**11 + 3, 1_000_001),
+                                            (20240601, 3, 777)])
+def test_z_fill_vs_oracle(cuda, oracle, seed, counter, n):
+    out = torch.empty(n, dtype=torch.float64, device=cuda)
+    L().call("zo2_z_fill", out.data_ptr(), n, seed, 0, counter, stream())
+    ref = oracle.gauss(seed, 0, counter, n)
+    got = out.cpu().numpy()
+    bad = np.nonzero(got.view(np.uint64) != ref.view(np.uint64))[0]
+    assert bad.size == 0, f"{bad.size} mismatches, first {bad[:5]} {got[bad[:3]]} {ref[bad[:3]]}"
+
+
+def test_raw_fill(cuda, golden):
+    for c in golden("rng.json")["raw"]:
+        out = torch.empty(c["n"], dtype=torch.int64, device=cuda)
+        L().call("zo2_raw_fill", out.data_ptr(), c["n"], c["seed"], c["stream"], c["counter"],
+                 stream())
+        assert [int(x) for x in out.cpu().numpy().view(np.uint64)] == c["out"]
+
+
+def test_init_matches_reference(cuda, golden):
+    from paper_2503_12668_b200.model import ModelSpec, init_module_, module_order, module_size
+    G = golden("toy.json")
+    spec = ModelSpec(*G["spec"])
+    z = golden("toy_f32.npz")
+    for m in module_order(spec):
+        n = module_size(spec, m)
+        if n == 0:
+            continue
+        out = torch.empty(n, dtype=torch.float32, device=cuda)
+        init_module_(spec, m, G["seed"], out)
+        assert np.array_equal(out.cpu().numpy(), z["init::" + m]), m
+
+
+# ------------------------------------------------------------------ K2
+def _ref_sequence(oracle, w, base, upd_coef, lrs, eps, rs, perturb=True):
+    w = w.copy()
+    if upd_coef is not None:
+        oracle.axpy_z(w, upd_coef, lrs, base)
+    if not perturb:
+        return w, None, None
+    wp = w.copy()
+    oracle.axpy_z(wp, eps, rs, base)
+    wm = wp.copy()
+    oracle.axpy_z(wm, -2.0 * eps, rs, base)
+    wf = wm.copy()
+    oracle.axpy_z(wf, eps, rs, base)
+    return wf, wp, wm
+
+
+def _bf16_bits(x: np.ndarray) -> np.ndarray:
+    return torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(torch.bfloat16).view(
+        torch.int16).numpy()
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("g", [0.0, 2.5])
+def test_update_perturb_linear_bit_exact(cuda, oracle, dtype, g):
+    _l = L()
+    n, base, lrs, rs, eps, lr = 10_003, 1_000_004, 0x1234, 0xBEEF, 1e-3, 1e-2
+    w = (np.random.default_rng(1).standard_normal(n) * 0.05).astype(dtype)
+    dev = torch.from_numpy(w.copy()).to(cuda)
+    d_g = torch.tensor([g], dtype=torch.float64, device=cuda)
+    plus = torch.empty(n, dtype=torch.float32, device=cuda)
+    minus = torch.empty(n, dtype=torch.float32, device=cuda)
+    segs = (_l.SegmentDesc * 2)()
+    segs[0].offset, segs[0].rows, segs[0].cols, segs[0].out_kind = 0, 1, 4000, _l.OUT_F32
+    segs[0].out_plus, segs[0].out_minus = plus.data_ptr(), minus.data_ptr()
+    segs[1].offset, segs[1].rows, segs[1].cols, segs[1].out_kind = 4000, 1, n - 4000, _l.OUT_F32
+    segs[1].out_plus, segs[1].out_minus = plus.data_ptr() + 4000 * 4, minus.data_ptr() + 4000 * 4
+    fmt = _l.F32 if dtype == np.float32 else _l.F64
+    _l.call("zo2_update_perturb", dev.data_ptr(), fmt, n, base, 1, d_g.data_ptr(), lr, lrs, 1,
+            eps, rs, segs, 2, None, stream())
+    wf, wp, wm = _ref_sequence(oracle, w, base, (-(lr * g)) if g != 0 else None, lrs, eps, rs)
+    assert np.array_equal(dev.cpu().numpy().view(np.uint8), wf.view(np.uint8))
+    assert np.array_equal(plus.cpu().numpy(), wp.astype(np.float32))
+    assert np.array_equal(minus.cpu().numpy(), wm.astype(np.float32))
+
+
+@pytest.mark.parametrize("split", [False, True])
+def test_update_perturb_transposed_operands(cuda, oracle, split):
+    _l = L()
+    rows, cols, base, lrs, rs, eps, lr, g = 72, 200, 4096, 11, 22, 1e-3, 1e-3, -1.25
+    n = rows * cols
+    w = (np.random.default_rng(2).standard_normal(n) * 0.05).astype(np.float32)
+    dev = torch.from_numpy(w.copy()).to(cuda)
+    d_g = torch.tensor([g], dtype=torch.float64, device=cuda)
+    ph, mh = (torch.empty(n, dtype=torch.bfloat16, device=cuda) for _ in range(2))
+    pl, ml = (torch.empty(n, dtype=torch.bfloat16, device=cuda) for _ in range(2))
+    segs = (_l.SegmentDesc * 1)()
+    s = segs[0]
+    s.offset, s.rows, s.cols = 0, rows, cols
+    s.out_kind = _l.OUT_SPLIT_T if split else _l.OUT_BF16_T
+    s.out_plus, s.out_minus, s.out_plus_lo, s.out_minus_lo = (
+        ph.data_ptr(), mh.data_ptr(), pl.data_ptr(), ml.data_ptr())
+    _l.call("zo2_update_perturb", dev.data_ptr(), _l.F32, n, base, 1, d_g.data_ptr(), lr, lrs, 1,
+            eps, rs, segs, 1, None, stream())
+    wf, wp, wm = _ref_sequence(oracle, w, base, -(lr * g), lrs, eps, rs)
+    assert np.array_equal(dev.cpu().numpy(), wf)
+    for ref, hi, lo in ((wp, ph, pl), (wm, mh, ml)):
+        refT = ref.reshape(rows, cols).T.copy()
+        hb = _bf16_bits(refT).reshape(-1)
+        assert np.array_equal(hi.view(torch.int16).cpu().numpy(), hb)
+        if split:
+            hif = hi.float().cpu().numpy().reshape(cols, rows)
+            assert np.array_equal(lo.view(torch.int16).cpu().numpy(),
+                                  _bf16_bits(refT - hif).reshape(-1))
+
+
+@pytest.mark.parametrize("codec", ["bf16", "f16", "f8"])
+def test_update_perturb_codec_arena(cuda, oracle, codec):
+    """Codec arena: decode -> f32 update/perturb/restore -> encode, in one pass
+    (runtime.py:172-184 + zo2_engine.py:183-204)."""
+    _l = L()
+    n, base, lrs, rs, eps, lr, g = 8192, 64, 5, 6, 1e-2, 1e-1, 3.0
+    w = (np.random.default_rng(3).standard_normal(n) * 0.5).astype(np.float32)
+    w[:4] = [np.nan, 1e6, -1e6, 0.0]
+    bits, _, _ = oracle.encode(w, codec)
+    fmt = {"bf16": _l.BF16, "f16": _l.F16, "f8": _l.F8E4M3}[codec]
+    dev = torch.from_numpy(bits.view(np.int16) if bits.dtype == np.uint16 else bits).to(cuda)
+    d_g = torch.tensor([g], dtype=torch.float64, device=cuda)
+    counts = torch.zeros(2, dtype=torch.int64, device=cuda)
+    segs = (_l.SegmentDesc * 1)()
+    segs[0].offset, segs[0].rows, segs[0].cols, segs[0].out_kind = 0, 1, n, _l.OUT_NONE
+    _l.call("zo2_update_perturb", dev.data_ptr(), fmt, n, base, 1, d_g.data_ptr(), lr, lrs, 1,
+            eps, rs, segs, 1, counts.data_ptr(), stream())
+    wide = oracle.decode(bits, codec)
+    wf, _, _ = _ref_sequence(oracle, wide, base, -(lr * g), lrs, eps, rs)
+    ref_bits, nan, sat = oracle.encode(wf, codec)
+    got = dev.cpu().numpy()
+    assert np.array_equal(got.view(ref_bits.dtype), ref_bits)
+    assert counts.cpu().tolist() == [nan, sat]
+
+
+def test_update_only_ungated(cuda, oracle):
+    _l = L()
+    n = 4096
+    w = np.random.default_rng(4).standard_normal(n).astype(np.float32)
+    for upd, g in ((1, 0.0), (2, 0.0), (2, 1.5)):
+        dev = torch.from_numpy(w.copy()).to(cuda)
+        d_g = torch.tensor([g], dtype=torch.float64, device=cuda)
+        segs = (_l.SegmentDesc * 1)()
+        segs[0].offset, segs[0].rows, segs[0].cols = 0, 1, n
+        _l.call("zo2_update_perturb", dev.data_ptr(), _l.F32, n, 0, upd, d_g.data_ptr(), 0.1, 9,
+                0, 1e-3, 0, segs, 1, None, stream())
+        ref = w.copy()
+        if upd == 2 or g != 0:
+            oracle.axpy_z(ref, -(0.1 * g), 9, 0)
+        assert np.array_equal(dev.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+# ------------------------------------------------------------------ K9
+@pytest.mark.parametrize("fmt", ["bf16", "f16", "f8"])
+def test_codecs_bit_exact(cuda, golden, fmt):
+    _l = L()
+    g = golden("codecs.npz")
+    x = torch.from_numpy(g["x"]).to(cuda)
+    code = {"bf16": _l.BF16, "f16": _l.F16, "f8": _l.F8E4M3}[fmt]
+    dt = torch.uint8 if fmt == "f8" else torch.int16
+    enc = torch.empty(x.numel(), dtype=dt, device=cuda)
+    counts = torch.zeros(2, dtype=torch.int64, device=cuda)
+    _l.call("zo2_encode", x.data_ptr(), enc.data_ptr(), code, x.numel(), counts.data_ptr(),
+            stream())
+    ref = g[f"{fmt}_bits"]
+    assert np.array_equal(enc.cpu().numpy().view(ref.dtype), ref)
+    assert counts.cpu().tolist() == g[f"{fmt}_counts"].tolist()
+    dec = torch.empty(x.numel(), dtype=torch.float32, device=cuda)
+    _l.call("zo2_decode", enc.data_ptr(), dec.data_ptr(), code, x.numel(), stream())
+    d, r = dec.cpu().numpy(), g[f"{fmt}_dec"]
+    assert ((d.view(np.uint32) == r.view(np.uint32)) | (np.isnan(d) & np.isnan(r))).all()
+
+
+# ------------------------------------------------------------------ K3 GEMM
+def _planes(x: torch.Tensor, split: bool):
+    hi = x.to(torch.bfloat16)
+    lo = (x - hi.float()).to(torch.bfloat16) if split else None
+    return hi.contiguous(), (lo.contiguous() if lo is not None else None)
+
+
+def _run_gemm(A, B, bias, epi, split, C=None, targets=None, n_tiles=None):
+    """A: [2, M, K] f32, B: [2, N, K] f32 -> runs the batch-2 kernel."""
+    _l = L()
+    _, M, K = A.shape
+    N = B.shape[1]
+    probs = (_l.GemmProblem * 2)()
+    keep = []
+    outs = []
+    for s in range(2):
+        ah, al = _planes(A[s], split)
+        bh, bl = _planes(B[s], split)
+        keep += [ah, al, bh, bl]
+        pr = probs[s]
+        pr.a_hi, pr.b_hi = ah.data_ptr(), bh.data_ptr()
+        pr.a_lo = al.data_ptr() if al is not None else None
+        pr.b_lo = bl.data_ptr() if bl is not None else None
+        pr.bias = bias[s].data_ptr() if bias is not None else None
+        if epi in (_l.EPI_STORE, _l.EPI_RESIDUAL):
+            c = C[s] if C is not None else torch.empty(M, N, device=A.device)
+            pr.c = c.data_ptr()
+            outs.append(c)
+        elif epi == _l.EPI_GELU:
+            ch = torch.empty(M, N, dtype=torch.bfloat16, device=A.device)
+            cl = torch.empty(M, N, dtype=torch.bfloat16, device=A.device)
+            pr.c, pr.c_lo = ch.data_ptr(), cl.data_ptr()
+            outs.append((ch, cl))
+        else:
+            part = torch.empty(M, n_tiles, 3, device=A.device)
+            pr.targets, pr.ce_part = targets.data_ptr(), part.data_ptr()
+            outs.append(part)
+    _l.call("zo2_gemm", probs, 2, M, N, K, epi, stream())
+    torch.cuda.synchronize()
+    return outs
+
+
+SHAPES = [(128, 256, 64), (32, 96, 32), (300, 520, 200), (1024, 768, 768), (2048, 3072, 1024)]
+
+
+@pytest.mark.parametrize("split", [False, True])
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_gemm_store_bias(cuda, split, M, N, K):
+    torch.manual_seed(0)
+    A = torch.randn(2, M, K, device=cuda)
+    B = torch.randn(2, N, K, device=cuda) * 0.05
+    bias = [torch.randn(N, device=cuda) for _ in range(2)]
+    outs = _run_gemm(A, B, bias, L().EPI_STORE, split)
+    for s in range(2):
+        if split:
+            ref = (A[s].double() @ B[s].double().T + bias[s].double()).float()
+            tol = 2e-5 * (A[s].abs().double() @ B[s].abs().double().T).max().item() + 1e-6
+        else:
+            ah, bh = A[s].to(torch.bfloat16).double(), B[s].to(torch.bfloat16).double()
+            ref = (ah @ bh.T + bias[s].double()).float()
+            tol = 1e-5 * (ah.abs() @ bh.abs().T).max().item() + 1e-6
+        err = (outs[s] - ref).abs().max().item()
+        assert err <= tol, (s, err, tol)
+
+
+@pytest.mark.parametrize("split", [False, True])
+def test_gemm_residual_and_gelu(cuda, split):
+    torch.manual_seed(1)
+    M, N, K = 384, 512, 256
+    A = torch.randn(2, M, K, device=cuda)
+    B = torch.randn(2, N, K, device=cuda) * 0.05
+    bias = [torch.randn(N, device=cuda) for _ in range(2)]
+    h0 = [torch.randn(M, N, device=cuda) for _ in range(2)]
+    C = [h.clone() for h in h0]
+    _run_gemm(A, B, bias, L().EPI_RESIDUAL, split, C=C)
+    g = _run_gemm(A, B, bias, L().EPI_GELU, split)
+    for s in range(2):
+        if split:
+            lin = A[s].double() @ B[s].double().T + bias[s].double()
+        else:
+            lin = (A[s].to(torch.bfloat16).double() @ B[s].to(torch.bfloat16).double().T
+                   + bias[s].double())
+        assert (C[s].double() - (h0[s].double() + lin)).abs().max().item() < 1e-4
+        gel = torch.nn.functional.gelu(lin)
+        ch, cl = g[s]
+        val = ch.double() + (cl.double() if split else 0)
+        tol = 1e-4 if split else 2e-2
+        assert (val - gel).abs().max().item() < tol * max(1.0, gel.abs().max().item())
+
+
+@pytest.mark.parametrize("split", [False, True])
+def test_gemm_cross_entropy(cuda, split):
+    torch.manual_seed(2)
+    _l = L()
+    M, N, K = 256, 1000, 128
+    A = torch.randn(2, M, K, device=cuda)
+    B = torch.randn(2, N, K, device=cuda) * 0.1
+    tgt = torch.randint(0, N, (M,), device=cuda)
+    tile = _l.load().zo2_gemm_tile_n(1 if split else 0)
+    nt = (N + tile - 1) // tile
+    parts = _run_gemm(A, B, None, _l.EPI_CE, split, targets=tgt, n_tiles=nt)
+    part_all = torch.stack(parts).contiguous()
+    sums = torch.zeros(2, dtype=torch.float64, device=cuda)
+    _l.call("zo2_ce_reduce", part_all.data_ptr(), M, nt, 2, M * nt * 3, sums.data_ptr(),
+            stream())
+    torch.cuda.synchronize()
+    for s in range(2):
+        if split:
+            logits = A[s].double() @ B[s].double().T
+        else:
+            logits = A[s].to(torch.bfloat16).double() @ B[s].to(torch.bfloat16).double().T
+        ref = (torch.logsumexp(logits, -1) - logits[torch.arange(M), tgt]).sum().item()
+        assert abs(sums[s].item() - ref) <= 1e-5 * abs(ref), (sums[s].item(), ref)
+
+
+# ------------------------------------------------------------------ LN / attention / embed
+@pytest.mark.parametrize("dim", [32, 768, 2048, 7168])
+def test_layernorm(cuda, dim):
+    rows = 64
+    x = torch.randn(rows, dim, device=cuda) * 3 + 1
+    g = torch.randn(dim, device=cuda)
+    b = torch.randn(dim, device=cuda)
+    hi = torch.empty(rows, dim, dtype=torch.bfloat16, device=cuda)
+    lo = torch.empty_like(hi)
+    L().call("zo2_layernorm", x.data_ptr(), rows, dim, g.data_ptr(), b.data_ptr(), hi.data_ptr(),
+             lo.data_ptr(), stream())
+    torch.cuda.synchronize()
+    xd = x.double()
+    mu = xd.mean(-1, keepdim=True)
+    var = ((xd - mu) ** 2).mean(-1, keepdim=True)
+    ref = (xd - mu) / torch.sqrt(var + 1e-5) * g.double() + b.double()
+    got = hi.double() + lo.double()
+    assert (got - ref).abs().max().item() < 2e-5 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("B,S,H,hd", [(2, 16, 4, 8), (2, 128, 12, 64), (1, 512, 4, 128)])
+def test_attention(cuda, B, S, H, hd):
+    d = H * hd
+    qkv = torch.randn(B * S, 3 * d, device=cuda)
+    hi = torch.empty(B * S, d, dtype=torch.bfloat16, device=cuda)
+    lo = torch.empty_like(hi)
+    L().call("zo2_attention", qkv.data_ptr(), B, S, H, hd, hi.data_ptr(), lo.data_ptr(), stream())
+    torch.cuda.synchronize()
+    q, k, v = (t.reshape(B, S, H, hd).transpose(1, 2).double() for t in qkv.split(d, -1))
+    sc = q @ k.transpose(-1, -2) / hd ** 0.5
+    mask = torch.tril(torch.ones(S, S, dtype=torch.bool, device=cuda))
+    sc = sc.masked_fill(~mask, float("-inf"))
+    ref = (torch.softmax(sc, -1) @ v).transpose(1, 2).reshape(B * S, d)
+    got = hi.double() + lo.double()
+    assert (got - ref).abs().max().item() < 2e-5
+
+
+def test_embed_dual_matches_oracle(cuda, oracle):
+    from paper_2503_12668_b200.model import ModelSpec
+    spec = ModelSpec(1, 32, 4, 64, 16)
+    p = oracle.init_params(oracle.Spec(1, 32, 4, 64, 16), 5)
+    table = p["embed"]
+    ids = np.random.default_rng(0).integers(0, 64, (3, 16))
+    lrs, rs, eps, lr, g = 101, 202, 1e-3, 1e-2, 0.7
+    dev = torch.from_numpy(table).to(cuda)
+    d_g = torch.tensor([g], dtype=torch.float64, device=cuda)
+    idt = torch.from_numpy(ids.reshape(-1)).to(cuda)
+    op = torch.empty(48 * 32, device=cuda)
+    om = torch.empty(48 * 32, device=cuda)
+    L().call("zo2_embed_dual", idt.data_ptr(), 48, 16, 32, 64, 16, dev.data_ptr(), 0, 1,
+             d_g.data_ptr(), lr, lrs, eps, rs, op.data_ptr(), om.data_ptr(), stream())
+    _, wp, wm = _ref_sequence(oracle, table, 0, -(lr * g), lrs, eps, rs)
+    for ref_flat, got in ((wp, op), (wm, om)):
+        v = oracle.views(ref_flat, oracle.layouts(oracle.Spec(1, 32, 4, 64, 16))["embed"])
+        ref = v["tok_emb"][ids] + v["pos_emb"][:16]
+        assert np.array_equal(got.cpu().numpy().reshape(3, 16, 32), ref)
