@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""ZO2 step throughput on B200 (BASELINE.json metric: "ZO step tokens/s
+(1/2/4/8 B200) vs PCIe/tensor roofline; H2D GB/s; GPU idle %").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+Workload (default cfg2 = BASELINE configs[1]): OPT-1.3B geometry (24 blocks,
+d 2048, 32 heads, V 50272), per-block offload, f32 parameters and f32 wire,
+batch 16 x 512 synthetic tokens per rank, random-init weights (init_params
+semantics, seed 1).  One "step" = one full ZO2 iteration (dual forward of
+every module with the deferred ZO-SGD update fused in, all 24 blocks
+uploaded and offloaded over PCIe).  Each step streams 4.8 GB of block
+weights per direction, far larger than the 126 MB L2 (no flush needed).
+
+value  device-timed (CUDA events, compute stream, max over ranks) with the
+       batch already resident in HBM, steps enqueued asynchronously.
+e2e    the public API Zo2Engine.step(batch) per step: pinned H2D of the
+       batch, D2H of (l+, l-, g), synchronous (wall clock == device here).
+--impl reference  the reference's CPU path (oracle port of zo2lab's step) on
+       the host cores, each step a bounded sample scaled to the full step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg2": dict(workload="OPT-1.3B ZO2 per-block offload fp32, batch 16 x seq 512",
+                 spec=(24, 2048, 32, 50272, 512), B=16, arith="f32", codec="none", lr=1e-7,
+                 slots=3),
+    "cfg3": dict(workload="OPT-6.7B ZO2 AMP: bf16 compute, bf16 wire, batch 16 x seq 512",
+                 spec=(32, 4096, 32, 50272, 512), B=16, arith="bf16", codec="bf16", lr=1e-7,
+                 slots=3),
+    "cfg3f16": dict(workload="OPT-6.7B ZO2 AMP: bf16 compute, fp16 wire, batch 16 x seq 512",
+                    spec=(32, 4096, 32, 50272, 512), B=16, arith="bf16", codec="f16", lr=1e-7,
+                    slots=3),
+    "cfg4": dict(workload="OPT-30B ZO2 offload, bf16 compute/wire, 18 GB HBM cap, 16 x 512",
+                 spec=(48, 7168, 56, 50272, 512), B=16, arith="bf16", codec="bf16", lr=1e-7,
+                 slots=3, cap=18e9),
+}
+EPS, SEED = 1e-3, 1
+
+_FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        d["source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    d = dict(_FALLBACK_PEAKS)
+    d["source"] = "fallback (B200_PROFILING.md)"
+    return d
+
+
+# ----------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ----------------------------------------------------------------------------
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc = index, None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 8:
+                self.rows.append(f)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------
+# CPU baseline: the reference's step (oracle port), bounded sample
+# ----------------------------------------------------------------------------
+_CPU_STATE: dict = {}
+
+
+def cpu_step_sample(spec_t, B, lr):
+    """Time the oracle's deferred ZO2 step pieces on this host and scale them to
+    one full step: per block = RNG passes (update + 3 perturb passes over 1/8
+    of the block, x32) + dual forward at batch 2 (x B/2); embed + head
+    likewise.  Returns (seconds per full step, sample description)."""
+    from oracle import zo2_oracle as O
+    nb, d, H, V, S = spec_t
+    spec = O.Spec(1, d, H, V, S)
+    key = (spec_t, B)
+    if key not in _CPU_STATE:  # setup (init + data) is not part of the sample
+        _CPU_STATE[key] = (O.init_params(spec, SEED), O.gen_synthetic(V, S, 4, SEED))
+    p, (tok, tgt) = _CPU_STATE[key]
+    bsub = 2
+    scale = B / bsub
+    tk, tg = tok[:bsub], tgt[:bsub]
+    blk = p["block.0"]
+    part = blk[: blk.size // 8].copy()
+    t0 = time.perf_counter()
+    for c in (-(lr * 1.0), EPS, -2 * EPS, EPS):
+        O.axpy_z(part, c, 12345, 0)
+    t_rng_block = (time.perf_counter() - t0) * 8
+    h = O.fwd_embed(spec, p["embed"], tk)
+    t0 = time.perf_counter()
+    for _ in range(2):
+        O.fwd_block(spec, blk, h)
+    t_fwd_block = (time.perf_counter() - t0) * scale
+    t0 = time.perf_counter()
+    for _ in range(2):
+        O.fwd_embed(spec, p["embed"], tk)
+    t_embed = (time.perf_counter() - t0) * scale
+    headw = p["head"].reshape(V, d)
+    t0 = time.perf_counter()
+    for _ in range(2):
+        O.ce_loss(h @ headw.T, tg)
+    t_head = (time.perf_counter() - t0) * scale
+    n_res = p["embed"].size + p["head"].size
+    t_rng_res = t_rng_block * n_res / blk.size
+    total = nb * (t_rng_block + t_fwd_block) + t_rng_res + t_embed + t_head
+    desc = (f"oracle ZO2 step pieces on host: 1 block RNG passes on 1/8 of the block (x32), "
+            f"1 block dual forward at batch {bsub}x{S} (x{scale:g}), embed+head dual forward "
+            f"at batch {bsub} (x{scale:g}), resident-module RNG scaled by size; "
+            f"estimate = {nb} x block + embed + head")
+    return total, desc
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        th = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:
+        th = os.cpu_count() or 1
+    return int(th)
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the reference's CPU path on this host (rank 0 only)."""
+    if rank != 0:
+        return
+    nb, d, H, V, S = cfg["spec"]
+    tokens = cfg["B"] * S
+    for _ in range(args.warmup):
+        cpu_step_sample(cfg["spec"], cfg["B"], cfg["lr"])
+    ts = []
+    desc = ""
+    for _ in range(args.steps):
+        t, desc = cpu_step_sample(cfg["spec"], cfg["B"], cfg["lr"])
+        ts.append(t)
+    step_s = statistics.median(ts)
+    value = tokens / step_s
+    line = {"impl": "reference", "metric": "ZO step tokens/s", "value": value,
+            "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "global_batch": cfg["B"], "seq_len": S,
+                       "model": "reference toy block at OPT geometry (random init)",
+                       "parallelism": "cpu"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_threads(),
+                             "kind": "port", "sample": desc},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+def run_ours(args, cfg, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_12668_b200 import _lib
+    from paper_2503_12668_b200.data import gen_synthetic
+    from paper_2503_12668_b200.engine import TransformerWorkload, ZOConfig, Zo2Engine
+    from paper_2503_12668_b200.model import ModelSpec
+    from paper_2503_12668_b200.numerics import RngState
+    from paper_2503_12668_b200.runtime import OffloadRuntime, init_params
+    from paper_2503_12668_b200.scheduler import Lane
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    nb, d, H, V, S = cfg["spec"]
+    spec = ModelSpec(nb, d, H, V, S)
+    B = cfg["B"]
+    T = B * S
+    params = init_params(spec, RngState(SEED), device=dev)
+    rt = OffloadRuntime(params, k_slots=cfg["slots"], codec=cfg["codec"],
+                        capacity_bytes=cfg.get("cap", float("inf")), device=dev)
+    eng = Zo2Engine(TransformerWorkload(params, cfg["arith"]),
+                    ZOConfig(EPS, cfg["lr"], max(1, args.steps), SEED), rt, validate=True)
+    if world > 1:
+        eng.enable_data_parallel()
+    ds = gen_synthetic(V, S, 64 * world, RngState(SEED), "affine", B)
+    from paper_2503_12668_b200.engine import batch_for_step
+
+    def batch(j):
+        idx = batch_for_step(SEED, j, ds.n_samples, B * world)[rank * B:(rank + 1) * B]
+        return ds.batch(idx)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    j = 0
+    for _ in range(args.warmup):
+        eng.step(batch(j), j)
+        j += 1
+    torch.cuda.synchronize()
+
+    # ---- value: device-timed, batch resident, async enqueue ----------------
+    lib = _lib.load()
+    comp = eng.lanes[Lane.COMPUTE]
+    eng.dev.fwd.prof = []
+    n_tl0 = len(eng.timelines)
+    barrier()
+    torch.cuda.synchronize()
+    l0 = lib.zo2_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local_rank) as clk:
+        e0.record(comp)
+        for k in range(args.steps):
+            eng.step_async(j + k)
+        e1.record(comp)
+        eng.drain()
+        torch.cuda.synchronize()
+    launches = lib.zo2_launch_count() - l0
+    barrier()
+    j += args.steps
+    dev_ms = e0.elapsed_time(e1)
+    # the last offload of the last step may end after the compute stream
+    tls = [tl for _, tl in eng.timelines[n_tl0:]]
+    ms = max_over_ranks(dev_ms)
+    prof = eng.dev.fwd.prof
+    eng.dev.fwd.prof = None
+    gemm = [(w, a.elapsed_time(b)) for kind, w, a, b in prof if kind == "gemm"]
+    k2 = [(w, a.elapsed_time(b)) for kind, w, a, b in prof if kind == "k2"]
+    gemm_flops = sum(w for w, _ in gemm)
+    gemm_ms = sum(t for _, t in gemm)
+    k2_ms = sum(t for _, t in k2)
+
+    # per-step timeline metrics: H2D GB/s from upload events, GPU idle %
+    up = [e for tl in tls for e in tl.events if e.lane is Lane.UPLOAD]
+    off = [e for tl in tls for e in tl.events if e.lane is Lane.OFFLOAD]
+    h2d_gbs = (sum(rt.block_nbytes for _ in up) / sum(e.duration for e in up) / 1e9) if up else None
+    d2h_gbs = (sum(rt.block_nbytes for _ in off) / sum(e.duration for e in off) / 1e9) if off else None
+    comp_busy = sum(tl.lane_busy(Lane.COMPUTE) for tl in tls)
+    idle_pct = max(0.0, 100.0 * (1.0 - comp_busy / (dev_ms * 1e-3))) if tls else None
+
+    # ---- e2e: public API per step (host batch in, (l+, l-, g) out) ---------
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        eng.step(batch(j + k), j + k)
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    barrier()
+
+    pk = peaks()
+    tokens_step = T * world
+    value = tokens_step * args.steps / (ms * 1e-3)
+    e2e_value = tokens_step * args.steps / e2e_s
+    wire_per_dir = nb * rt.block_nbytes
+    # step roofline: slower of offloaded bytes at the measured
+    # host link and algorithmic GEMM FLOPs at the bf16 tensor peak
+    flops_step = 2 * (nb * (24.0 * T * d * d + 4.0 * B * S * S * d) + 2.0 * T * d * V)
+    t_link = wire_per_dir / (h2d_gbs * 1e9) if h2d_gbs else None
+    t_tensor = flops_step / (pk["bf16_tflops_sustained"] * 1e12)
+    t_roof = max(t_link or 0.0, t_tensor)
+    step_s = ms * 1e-3 / args.steps
+    gemm_tflops = gemm_flops / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None
+    split = cfg["arith"] == "f32"
+    line = {
+        "metric": "ZO step tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if split else "bf16", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "model": f"OPT geometry {nb}x{d}, V={V}",
+                   "global_batch": B * world, "seq_len": S,
+                   "parallelism": f"dp{world}" if world > 1 else "single",
+                   "wire": cfg["codec"] if cfg["codec"] != "none" else "f32",
+                   "compute": "3-pass bf16 split GEMM (f32-faithful)" if split else "bf16 GEMM",
+                   "l2": "inputs larger than L2 (4.8+ GB of weights streamed per step)"},
+        "roofline": {"bound": "tensor", "kernel": "zo2_gemm (tcgen05, fused epilogues)",
+                     "achieved": gemm_tflops, "peak": pk["bf16_tflops_sustained"],
+                     "unit": "TFLOP/s", "frac": (gemm_tflops / pk["bf16_tflops_sustained"]
+                                                 if gemm_tflops else None),
+                     "traffic": None, "peak_source": pk["source"] + ", sustained",
+                     "algorithmic": "2*M*N*K per problem (x3 tensor passes when split)",
+                     "gemm_ms_per_step": gemm_ms / args.steps,
+                     "k2_ms_per_step": k2_ms / args.steps},
+        "step_roofline": {"bound": "pcie" if (t_link or 0) >= t_tensor else "tensor",
+                          "h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs,
+                          "bytes_per_dir": wire_per_dir, "t_link_ms": (t_link or 0) * 1e3,
+                          "t_tensor_ms": t_tensor * 1e3, "frac": t_roof / step_s},
+        "gpu_idle_pct": idle_pct,
+        "e2e": {"value": e2e_value, "unit": "tokens/s",
+                "h2d_bytes_per_step": 2 * T * 8 + wire_per_dir,
+                "d2h_bytes_per_step": 4 * 8 + wire_per_dir,
+                "note": "h2d/d2h include the per-step block weight traffic of the offload"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "losses_tail": eng.losses[-2:],
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ts = []
+        desc = ""
+        for _ in range(3):
+            t, desc = cpu_step_sample(cfg["spec"], B, cfg["lr"])
+            ts.append(t)
+        cs = statistics.median(ts)
+        line["cpu_baseline"] = {"value": T / cs, "unit": "tokens/s", "cores": cpu_threads(),
+                                "kind": "port", "sample": desc}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -216,7 +216,12 @@ __device__ __forceinline__ uint16_t enc_f16(float x, unsigned &nn, unsigned &ns)
   }
   return h;
 }
+// f16 -> f32 widening; NaN payloads are kept (mantissa << 13) as numpy's
+// astype does, so a decode/encode round trip is the identity.
 __device__ __forceinline__ float dec_f16(uint16_t b) {
+  if ((b & 0x7C00u) == 0x7C00u && (b & 0x3FFu))
+    return __uint_as_float(((uint32_t)(b & 0x8000u) << 16) | 0x7F800000u |
+                           ((uint32_t)(b & 0x3FFu) << 13));
   return __half2float(__ushort_as_half(b));
 }
 // e4m3 (numerics.py:248-270), evaluated in double exactly as the reference.
@@ -431,12 +436,22 @@ template <> struct Wire<ZO2_F8E4M3> {
   }
 };
 
-// One axpy rounding (model.py:233): store(f64(w) + coef*z).
+// One axpy rounding (model.py:233): store(f64(w) + coef*z).  NaN handling
+// follows the reference's x86 SSE arithmetic, not CUDA's canonical NaN: a NaN
+// weight propagates its own (quieted) payload, an invalid operation yields
+// the x86 default NaN (sign set) -- visible through the f16 codec.
 __device__ __forceinline__ float axpy1(float w, double coef, double z) {
-  return __double2float_rn(__dadd_rn((double)w, __dmul_rn(coef, z)));
+  if (w != w) return __uint_as_float(__float_as_uint(w) | 0x00400000u);
+  const double s = __dadd_rn((double)w, __dmul_rn(coef, z));
+  if (s != s) return __uint_as_float(0xFFC00000u);
+  return __double2float_rn(s);
 }
 __device__ __forceinline__ double axpy1(double w, double coef, double z) {
-  return __dadd_rn(w, __dmul_rn(coef, z));
+  if (w != w)
+    return __longlong_as_double(__double_as_longlong(w) | 0x0008000000000000LL);
+  const double s = __dadd_rn(w, __dmul_rn(coef, z));
+  if (s != s) return __longlong_as_double((long long)0xFFF8000000000000ULL);
+  return s;
 }
 
 struct K2Params {

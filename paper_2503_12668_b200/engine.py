@@ -230,8 +230,20 @@ class Zo2Engine:
         self._blocks = [m for m in self._order if self._handles[m].transferable]
         self.lanes = CudaLanes(runtime.device)
         self.dev = _DeviceStep(workload.spec, workload.arith, runtime.device)
-        self._lrs_seed_of: dict[str, int] = {}
         self._pool_booked = False
+        self._async: list = []
+        self._hist = torch.zeros(64, 4, dtype=torch.float64, device=runtime.device)
+        # data parallel: loss sums are all-reduced before g is formed (K10)
+        self.dist_group = None
+        self.world = 1
+
+    def enable_data_parallel(self, group=None) -> None:
+        """Shard the batch over torch.distributed ranks: every rank perturbs with
+        the same seed and applies the same g; only the two f64 loss sums cross
+        NVLink (one NCCL all-reduce per step on the compute stream)."""
+        import torch.distributed as dist
+        self.dist_group = group or dist.group.WORLD
+        self.world = dist.get_world_size(self.dist_group)
 
     # -- bookkeeping of one module visit (zo2_engine.py:187-203) -------------
     def _visit(self, module: str, step: int) -> tuple[RngState, RngState | None, bool]:
@@ -259,10 +271,18 @@ class Zo2Engine:
         n = self._handles[module].size
         if n == 0:
             return
+        prof = self.dev.fwd.prof if self.dev.fwd is not None else None
+        if prof is not None:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
         _lib.call("zo2_update_perturb", buf.data_ptr(), fmt_code, n, self.dev.offsets[module],
                   int(update), self.dev.d_out[2:].data_ptr(), self.cfg.lr, lrs_seed,
                   int(perturb), self.cfg.eps, rs_seed, descs, len(descs),
                   self.runtime.d_conv.data_ptr(), stream.cuda_stream)
+        if prof is not None:
+            e1.record(stream)
+            # work unit: Gaussian draws regenerated (update pass + perturb pass)
+            prof.append(("k2", float(n * ((1 if update else 0) + (1 if perturb else 0))), e0, e1))
 
     # -- per-module compute tasks -------------------------------------------
     def _compute(self, module: str, step: int, seq: int, stream: torch.cuda.Stream) -> None:
@@ -288,8 +308,12 @@ class Zo2Engine:
             self._k2(self.runtime.persistent[HEAD_ID], _lib.F32, module, update, lrs_seed, True,
                      rs.seed, fwd.head_descs(), stream)
             fwd.head_forward(s)
-            _lib.call("zo2_form_g", fwd.d_sums.data_ptr(), float(fwd.T), self.cfg.eps,
-                      self.dev.d_out.data_ptr(), self.dev.d_flag.data_ptr(), s)
+            if self.dist_group is not None:
+                import torch.distributed as dist
+                with torch.cuda.stream(stream):
+                    dist.all_reduce(fwd.d_sums, group=self.dist_group)
+            _lib.call("zo2_form_g", fwd.d_sums.data_ptr(), float(fwd.T * self.world),
+                      self.cfg.eps, self.dev.d_out.data_ptr(), self.dev.d_flag.data_ptr(), s)
         else:
             slot = self.runtime.slot_for(self._blocks.index(module))
             self._k2(self.runtime.slot_bucket(slot), self.runtime.wire_fmt.code, module, update,
@@ -330,11 +354,68 @@ class Zo2Engine:
 
     # -- one iteration (zo2_engine.py:264-316) --------------------------------
     def step(self, batch, step_index: int) -> float:
+        """Reference contract: enqueue the whole iteration, synchronise, return g."""
+        enq, dag, recs = self._enqueue(batch, step_index)
+        self.dev.read_out(self.lanes[Lane.COMPUTE])
+        self.lanes.synchronize()
+        lp, lm, g, flag = (float(x) for x in self.dev.h_out.tolist())
+        return self._finish(step_index, enq, dag, recs, lp, lm, g, flag)
+
+    def step_async(self, step_index: int, batch=None) -> None:
+        """Enqueue one iteration without waiting (device-resident batch when
+        `batch` is None).  The next iteration's deferred update reads g from
+        HBM and is gated on g != 0 on the device; drain() synchronises and
+        performs the per-step checks of step()."""
+        enq, dag, recs = self._enqueue(batch, step_index)
+        slot = len(self._async)
+        if slot >= self._hist.shape[0]:
+            raise RuntimeError("too many outstanding async steps; call drain()")
+        with torch.cuda.stream(self.lanes[Lane.COMPUTE]):
+            self._hist[slot, :3].copy_(self.dev.d_out)
+            self._hist[slot, 3:4].copy_(self.dev.d_flag.to(torch.float64))
+        self._async.append((step_index, enq, dag, recs))
+        if self.update_mode != "naive":
+            self.pending.valid, self.pending.g = True, float("nan")  # resolved on device
+
+    def drain(self) -> list[float]:
+        self.lanes.synchronize()
+        hist = self._hist[: len(self._async)].cpu().tolist()
+        gs = []
+        for (j, enq, dag, recs), (lp, lm, g, flag) in zip(self._async, hist):
+            gs.append(self._finish(j, enq, dag, recs, lp, lm, g, flag))
+        self._async.clear()
+        return gs
+
+    def _finish(self, step_index, enq, dag, recs, lp, lm, g, flag) -> float:
+        timeline = enq.timeline()
+        self.runtime.commit_records(timeline, recs)
+        if flag != 0.0 or not (math.isfinite(lp) and math.isfinite(lm)):
+            raise NonFiniteLossError(f"step {step_index}: l+={lp}, l-={lm}")
+        if self.validate:
+            bad = validate_timeline(timeline, dag, tol=2e-6)
+            if bad:
+                raise SchedulingContractError("; ".join(str(v) for v in bad[:5]))
+        self.timelines.append((step_index, timeline))
+        if self.update_mode == "naive":
+            self.pending.clear()
+        else:
+            self.pending.set(g)
+        self.losses.append(lp)
+        self.losses_minus.append(lm)
+        self.gs.append(g)
+        return g
+
+    def _enqueue(self, batch, step_index: int):
         cfg, rt = self.cfg, self.runtime
         rt.current_step = step_index
         self.mgr.begin_iteration(derive_step_seed(cfg.seed, step_index))
         comp = self.lanes[Lane.COMPUTE]
-        _, seq = self.dev.stage_batch(batch, comp)
+        if batch is not None:
+            _, seq = self.dev.stage_batch(batch, comp)
+        elif self.dev.fwd is None:
+            raise ValueError("step_async(batch=None) needs a batch staged by an earlier step")
+        else:
+            seq = self.workload.spec.seq_len
         self._book_pool(self.dev.fwd)
         naive = self.update_mode == "naive"
         wire = {b: rt.block_nbytes for b in self._blocks}
@@ -356,30 +437,11 @@ class Zo2Engine:
             for m in self._order:
                 fns[ckey(m, 2)] = lambda st, m=m: self._naive_update(m, step_index, st)
         enq = enqueue_dag(dag, self.lanes, fns)
-        self.dev.read_out(comp)
-        self.lanes.synchronize()
-        timeline = enq.timeline()
-        rt.commit_records(timeline)
-        lp, lm, g, flag = (float(x) for x in self.dev.h_out.tolist())
-        if flag != 0.0 or not (math.isfinite(lp) and math.isfinite(lm)):
-            raise NonFiniteLossError(f"step {step_index}: l+={lp}, l-={lm}")
-        if self.validate:
-            bad = validate_timeline(timeline, dag, tol=2e-6)
-            if bad:
-                raise SchedulingContractError("; ".join(str(v) for v in bad[:5]))
-        self.timelines.append((step_index, timeline))
-        if naive:
-            self.pending.clear()
-        else:
-            self.pending.set(g)
         expected = 0 if naive else len(self._order)
         if len(self.mgr.rsb) != expected:
             raise StateCorruptionError(f"rsb holds {len(self.mgr.rsb)} entries, "
                                        f"expected {expected}")
-        self.losses.append(lp)
-        self.losses_minus.append(lm)
-        self.gs.append(g)
-        return g
+        return enq, dag, rt.take_records()
 
     def force_pending(self, g: float) -> None:
         """Parity hook: replace the pending projected gradient with an

@@ -234,6 +234,8 @@ class DualForward:
         self.ce_all = torch.empty(2, T * self.n_tiles_v * 3, dtype=torch.float32, device=dev)
         self.ce_part = [self.ce_all[0], self.ce_all[1]]
         self.d_sums = torch.zeros(2, dtype=torch.float64, device=dev)
+        # optional live kernel timing: list of (kind, work, start_evt, end_evt)
+        self.prof: list | None = None
         self.ids = torch.empty(T, dtype=torch.int64, device=dev)
         self.targets = torch.empty(T, dtype=torch.int64, device=dev)
         self._seg_cache: dict = {}
@@ -319,6 +321,15 @@ class DualForward:
             pr.c_lo = c_lo[s] if c_lo is not None else None
             pr.targets = targets.data_ptr() if targets is not None else None
             pr.ce_part = ce[s].data_ptr() if ce is not None else None
+        if self.prof is not None:
+            st = torch.cuda.ExternalStream(stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            _lib.call("zo2_gemm", probs, 2, M, N, K, epi, stream)
+            e1.record(st)
+            # algorithmic work of this launch: 2 problems x 2MNK flops
+            self.prof.append(("gemm", 2 * 2.0 * M * N * K, e0, e1))
+            return
         _lib.call("zo2_gemm", probs, 2, M, N, K, epi, stream)
 
     def embed_forward(self, table: torch.Tensor, base: int, update: bool, d_g, lr: float,

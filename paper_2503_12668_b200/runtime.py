@@ -276,14 +276,17 @@ class OffloadRuntime:
         rec = TransferRecord(module, "offload", self.block_nbytes, self.wire_fmt, 0.0, 0.0, step)
         self._pending_records.append((rec, key or f"O:{module}"))
 
-    def commit_records(self, timeline) -> None:
-        """Stamp the step's transfer records with device times and log them."""
+    def take_records(self) -> list:
+        out, self._pending_records = self._pending_records, []
+        return out
+
+    def commit_records(self, timeline, records=None) -> None:
+        """Stamp a step's transfer records with device times and log them."""
         ev = timeline.by_key()
-        for rec, key in self._pending_records:
+        for rec, key in (self.take_records() if records is None else records):
             if key in ev:
                 rec.t_start, rec.t_end = ev[key].t_start, ev[key].t_end
             self.log.append(rec)
-        self._pending_records.clear()
         nan, sat = (int(x) for x in self.d_conv.tolist())
         self.conversion.nan_count, self.conversion.saturated_count = nan, sat
 
