@@ -221,15 +221,15 @@ def run_ours(args, cfg, rank, world, local_rank):
     rt = OffloadRuntime(params, k_slots=cfg["slots"], codec=cfg["codec"],
                         capacity_bytes=cfg.get("cap", float("inf")), device=dev)
     eng = Zo2Engine(TransformerWorkload(params, cfg["arith"]),
-                    ZOConfig(EPS, cfg["lr"], max(1, args.steps), SEED), rt, validate=True)
+                    ZOConfig(EPS, cfg["lr"], max(1, args.steps), SEED), rt, validate=True,
+                    operand_sets=args.operand_sets)
     if world > 1:
         eng.enable_data_parallel()
     ds = gen_synthetic(V, S, 64 * world, RngState(SEED), "affine", B)
-    from paper_2503_12668_b200.engine import batch_for_step
+    from paper_2503_12668_b200.parallel import shard_indices
 
     def batch(j):
-        idx = batch_for_step(SEED, j, ds.n_samples, B * world)[rank * B:(rank + 1) * B]
-        return ds.batch(idx)
+        return ds.batch(shard_indices(SEED, j, ds.n_samples, B, rank, world))
 
     def barrier():
         if world > 1:
@@ -364,6 +364,8 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--operand-sets", type=int, default=1,
+                    help="1: K2 of block i+1 after the forward of block i; 2: concurrent")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -114,6 +114,10 @@ typedef struct zo2_segment_desc {
  * (naive-mode update pass, finalize drain).  codec conversions tally into
  * d_conv_counts[0] (NaN) and [1] (saturated) if non-null (ConversionSummary,
  * numerics.py:210-217). */
+/* Grid sizing of K2 (148 x n CTAs).  The engine sets 1 when K2 runs on the
+ * prepare stream concurrently with the GEMMs, so one K2 CTA and the persistent
+ * GEMM CTA co-reside on every SM (FP64/INT pipes vs tensor pipe). */
+int zo2_set_k2_ctas_per_sm(int n);
 int zo2_update_perturb(void *arena, int wire_fmt, uint64_t n, uint64_t base,
                        int update, const double *d_g, double lr,
                        uint64_t lrs_seed, int perturb, double eps,
@@ -187,10 +191,13 @@ int zo2_gemm(const zo2_gemm_problem *probs, int batch, uint32_t M, uint32_t N,
 int zo2_gemm_tile_n(int split);
 
 /* Combine CE partials into per-problem token sums (f64): sums[b] =
- * sum_t (logsumexp_t - logit_t[target_t])  (model.py:304-313 numerator). */
+ * sum_t (logsumexp_t - logit_t[target_t])  (model.py:304-313 numerator).
+ * Fixed-order two-phase reduction (bitwise reproducible); d_work holds
+ * batch * ZO2_CE_PARTS doubles. */
+#define ZO2_CE_PARTS 148
 int zo2_ce_reduce(const float *ce_part, uint32_t M, uint32_t n_tiles,
-                  int batch, uint64_t part_stride, double *d_sums,
-                  void *cuda_stream);
+                  int batch, uint64_t part_stride, double *d_work,
+                  double *d_sums, void *cuda_stream);
 
 /* model.py:273-283 causal softmax attention on packed qkv (f32 [B*S, 3d],
  * heads split as reshape(B,S,H,hd)), writing ctx as an A operand. */

@@ -23,6 +23,7 @@ F64, F32, F16, BF16, F8E4M3 = 0, 1, 2, 3, 4
 
 OUT_NONE, OUT_F32, OUT_BF16_T, OUT_SPLIT_T, OUT_BF16, OUT_SPLIT = 0, 1, 2, 3, 4, 5
 EPI_STORE, EPI_RESIDUAL, EPI_GELU, EPI_CE = 0, 1, 2, 3
+CE_PARTS = 148
 
 
 class SegmentDesc(ctypes.Structure):
@@ -55,7 +56,8 @@ _SIGS = {
     "zo2_update_perturb": (c_int, [c_void_p, c_int, c_uint64, c_uint64, c_int, c_void_p,
                                    c_double, c_uint64, c_int, c_double, c_uint64,
                                    POINTER(SegmentDesc), c_int, c_void_p, c_void_p]),
-    "zo2_encode": (c_int, [c_void_p, c_void_p, c_int, c_uint64, c_void_p, c_void_p]),
+    "zo2_set_k2_ctas_per_sm": (c_int, [c_int]),
+    "zo2_encode": (c_int,[c_void_p, c_void_p, c_int, c_uint64, c_void_p, c_void_p]),
     "zo2_decode": (c_int, [c_void_p, c_void_p, c_int, c_uint64, c_void_p]),
     "zo2_form_g": (c_int, [c_void_p, c_double, c_double, c_void_p, c_void_p, c_void_p]),
     "zo2_embed_dual": (c_int, [c_void_p, c_uint64, c_uint32, c_uint32, c_uint32, c_uint32,
@@ -68,7 +70,7 @@ _SIGS = {
                          c_void_p]),
     "zo2_gemm_tile_n": (c_int, [c_int]),
     "zo2_ce_reduce": (c_int, [c_void_p, c_uint32, c_uint32, c_int, c_uint64, c_void_p,
-                              c_void_p]),
+                              c_void_p, c_void_p]),
     "zo2_attention": (c_int, [c_void_p, c_uint32, c_uint32, c_uint32, c_uint32, c_void_p,
                               c_void_p, c_void_p]),
 }

@@ -6,11 +6,21 @@
 // vectors, grids are sized in multiples of the 148 SMs.
 #include "zo2_common.cuh"
 #include "zo2_rng.h"
+#include "zo2_zgen.cuh"
 #include <atomic>
 #include <string.h>
 #include <stdio.h>
 
 static std::atomic<uint64_t> g_launches{0};
+// K2 grid = 148 x this; 1 leaves room on every SM for the persistent GEMM CTA
+// when the prepare lane runs concurrently with the compute lane
+static unsigned g_k2_ctas_per_sm = 2;
+
+extern "C" int zo2_set_k2_ctas_per_sm(int n) {
+  if (n < 1 || n > 32) return zo2_set_error(ZO2_E_ARG, "zo2_set_k2_ctas_per_sm: 1..32");
+  g_k2_ctas_per_sm = (unsigned)n;
+  return ZO2_OK;
+}
 static thread_local char g_err[512] = "";
 
 extern "C" const char *zo2_last_error(void) { return g_err; }
@@ -464,30 +474,52 @@ struct K2Params {
   uint64_t rs_seed;
 };
 
-// Applies the per-module op sequence to 4 consecutive elements at bucket
-// index i (RNG positions base+i ..), returning W+ / W- in wp/wm.
-template <typename A>
-__device__ __forceinline__ void k2_math4(A w[4], A wp[4], A wm[4], uint64_t i,
-                                         const K2Params &P, int cnt) {
-  double z[4];
-  if (P.do_update) {
-    if (cnt == 4) z4_at(P.lrs_seed, ZO2_PERTURB_STREAM, P.base + i, z);
-    else
-      for (int j = 0; j < cnt; ++j) z[j] = zo2_gauss_at(P.lrs_seed, ZO2_PERTURB_STREAM, P.base + i + j);
-    for (int j = 0; j < cnt; ++j) w[j] = axpy1(w[j], P.ucoef, z[j]);
-  }
-  if (P.do_perturb) {
-    if (cnt == 4) z4_at(P.rs_seed, ZO2_PERTURB_STREAM, P.base + i, z);
-    else
-      for (int j = 0; j < cnt; ++j) z[j] = zo2_gauss_at(P.rs_seed, ZO2_PERTURB_STREAM, P.base + i + j);
-    const double m2 = -2.0 * P.eps;
-    for (int j = 0; j < cnt; ++j) {
-      wp[j] = axpy1(w[j], P.eps, z[j]);
-      wm[j] = axpy1(wp[j], m2, z[j]);
-      w[j] = axpy1(wm[j], P.eps, z[j]);
+// Applies the per-module op sequence to NQ quads of 4 consecutive elements at
+// bucket indices idx[q] (RNG positions base+idx[q] ..): deferred update with
+// z(lrs) if UPD, then +eps / -2eps / +eps with z(rs) if PERT, returning W+ /
+// W- in wp/wm.  cnt[q] = valid elements of quad q (0: inactive lane slot --
+// the lane still joins the warp-cooperative z evaluation).
+template <typename A, int NQ, bool UPD, bool PERT>
+__device__ __forceinline__ void k2_quads(A (&w)[NQ][4], A (&wp)[NQ][4], A (&wm)[NQ][4],
+                                         const uint64_t (&idx)[NQ], const int (&cnt)[NQ],
+                                         const K2Params &P,
+                                         ZgenScratch<NQ *((UPD ? 4 : 0) + (PERT ? 4 : 0))> &sc) {
+  constexpr int PER = (UPD ? 4 : 0) + (PERT ? 4 : 0);
+  constexpr int OFF = UPD ? 4 : 0;
+  double u[NQ * PER], z[NQ * PER];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    uint64_t r[4];
+    if (UPD) {
+      if (cnt[q] > 0) zo2_raw4(P.lrs_seed, ZO2_PERTURB_STREAM, P.base + idx[q], r);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) u[q * PER + j] = j < cnt[q] ? zo2_u53(r[j]) : 0.5;
     }
-  } else {
-    for (int j = 0; j < cnt; ++j) wp[j] = wm[j] = w[j];
+    if (PERT) {
+      if (cnt[q] > 0) zo2_raw4(P.rs_seed, ZO2_PERTURB_STREAM, P.base + idx[q], r);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) u[q * PER + OFF + j] = j < cnt[q] ? zo2_u53(r[j]) : 0.5;
+    }
+  }
+  warp_ndtri<NQ * PER>(u, z, sc);
+  const double m2 = -2.0 * P.eps;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j >= cnt[q]) continue;
+      A x = w[q][j];
+      if (UPD) x = axpy1(x, P.ucoef, z[q * PER + j]);
+      if (PERT) {
+        const double zr = z[q * PER + OFF + j];
+        wp[q][j] = axpy1(x, P.eps, zr);
+        wm[q][j] = axpy1(wp[q][j], m2, zr);
+        x = axpy1(wm[q][j], P.eps, zr);
+      } else {
+        wp[q][j] = wm[q][j] = x;
+      }
+      w[q][j] = x;
+    }
   }
 }
 
@@ -530,6 +562,8 @@ __device__ __forceinline__ void emit_linear(const zo2_segment_desc &sg, uint64_t
 }
 
 #define ZO2_MAX_SEGS 16
+// quads (4 columns) per lane in the transposing K2: warp tile = 32 rows x 4*TQ cols
+constexpr int TQ = 1;
 struct SegTable {
   zo2_segment_desc s[ZO2_MAX_SEGS];
   uint64_t quad_start[ZO2_MAX_SEGS + 1];  // prefix of 4-element chunks (linear kernel)
@@ -549,125 +583,133 @@ __device__ __forceinline__ double resolve_ucoef(const double *d_g, double lr, in
   return -(lr * g);
 }
 
-// Linear (same-layout) segments: one thread = 4 consecutive elements.
-template <int FMT>
-__global__ void __launch_bounds__(256) k_update_perturb_linear(
-    void *arena, SegTable T, K2Params P, const double *d_g, double lr, uint64_t *counts) {
+// Linear (same-layout) segments: one thread = 4 consecutive elements; the loop
+// advances whole warps so warp_ndtri always sees 32 converged lanes.
+template <int FMT, bool UPD, bool PERT>
+__device__ __forceinline__ void k2_linear_body(void *arena, const SegTable &T, const K2Params &P,
+                                               unsigned &nn, unsigned &ns, uint8_t *raw) {
   typedef typename Wire<FMT>::A A;
-  int upd = P.do_update;
-  P.ucoef = resolve_ucoef(d_g, lr, upd);
-  P.do_update = upd;
-  unsigned nn = 0, ns = 0;
+  constexpr int PER = (UPD ? 4 : 0) + (PERT ? 4 : 0);
+  ZgenScratch<PER> &sc = ((ZgenScratch<PER> *)raw)[threadIdx.x / 32];
   const uint64_t total = T.quad_start[T.n];
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t q = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; q < total; q += stride) {
+  for (uint64_t qb = blockIdx.x * (uint64_t)blockDim.x + (threadIdx.x & ~31u); qb < total;
+       qb += stride) {
+    const uint64_t q = qb + (threadIdx.x & 31u);
     int si = 0;
-    while (q >= T.quad_start[si + 1]) ++si;
-    const zo2_segment_desc &sg = T.s[si];
-    const uint64_t seg_n = (uint64_t)sg.rows * sg.cols;
-    const uint64_t li = (q - T.quad_start[si]) * 4;
-    const uint64_t i = sg.offset + li;
-    const int cnt = (int)min((uint64_t)4, seg_n - li);
-    A w[4], wp[4], wm[4];
-    const bool vec = cnt == 4 && (i & 3) == 0;
-    if (vec) Wire<FMT>::load4(arena, i, w);
+    uint64_t li = 0, i = 0;
+    int cnt[1] = {0};
+    if (q < total) {
+      while (q >= T.quad_start[si + 1]) ++si;
+      const uint64_t seg_n = (uint64_t)T.s[si].rows * T.s[si].cols;
+      li = (q - T.quad_start[si]) * 4;
+      i = T.s[si].offset + li;
+      cnt[0] = (int)min((uint64_t)4, seg_n - li);
+    }
+    A w[1][4], wp[1][4], wm[1][4];
+    const uint64_t idx[1] = {i};
+    const bool vec = cnt[0] == 4 && (i & 3) == 0;
+    if (vec) Wire<FMT>::load4(arena, i, w[0]);
     else
-      for (int j = 0; j < cnt; ++j) w[j] = Wire<FMT>::load1(arena, i + j);
-    k2_math4<A>(w, wp, wm, i, P, cnt);
-    if (vec) Wire<FMT>::store4(arena, i, w, nn, ns);
+      for (int j = 0; j < cnt[0]; ++j) w[0][j] = Wire<FMT>::load1(arena, i + j);
+    k2_quads<A, 1, UPD, PERT>(w, wp, wm, idx, cnt, P, sc);
+    if (cnt[0] == 0) continue;
+    if (vec) Wire<FMT>::store4(arena, i, w[0], nn, ns);
     else
-      for (int j = 0; j < cnt; ++j) Wire<FMT>::store1(arena, i + j, w[j], nn, ns);
-    if (P.do_perturb) emit_linear<A>(sg, li, wp, wm, cnt);
+      for (int j = 0; j < cnt[0]; ++j) Wire<FMT>::store1(arena, i + j, w[0][j], nn, ns);
+    if (PERT) emit_linear<A>(T.s[si], li, wp[0], wm[0], cnt[0]);
   }
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(256, 2) k_update_perturb_linear(
+    void *arena, SegTable T, K2Params P, const double *d_g, double lr, uint64_t *counts) {
+  int upd = P.do_update;
+  P.ucoef = resolve_ucoef(d_g, lr, upd);
+  unsigned nn = 0, ns = 0;
+  __shared__ __align__(16) uint8_t raw[8 * sizeof(ZgenScratch<8>)];
+  if (upd && P.do_perturb) k2_linear_body<FMT, true, true>(arena, T, P, nn, ns, raw);
+  else if (upd) k2_linear_body<FMT, true, false>(arena, T, P, nn, ns, raw);
+  else if (P.do_perturb) k2_linear_body<FMT, false, true>(arena, T, P, nn, ns, raw);
   if (FMT != ZO2_F32 && FMT != ZO2_F64) add_counts(counts, nn, ns);
 }
 
-// Transposed segments ([rows=K, cols=N] -> operand [N, K]) in 64x64 tiles.
-template <int FMT>
-__global__ void __launch_bounds__(256) k_update_perturb_transpose(
-    void *arena, SegTable T, K2Params P, const double *d_g, double lr, uint64_t *counts) {
+// Transposed segments ([rows=K, cols=N] -> operand [N, K]), shared-memory
+// free so it co-resides with the persistent GEMM on the same SMs (the GEMM
+// keeps the tensor pipe busy, this kernel the FP64/INT pipes).  Warp tile =
+// 32 rows x 8 cols: lane t owns row r0+t, cols c0..c0+7 (two Philox blocks
+// per stream); for each column the warp writes operand row n = c0+j over
+// K = r0..r0+31 as one coalesced 64-byte store.
+template <int FMT, bool UPD, bool PERT>
+__device__ __forceinline__ void k2_transpose_body(void *arena, const SegTable &T,
+                                                  const K2Params &P, unsigned &nn, unsigned &ns,
+                                                  uint8_t *raw) {
   typedef typename Wire<FMT>::A A;
-  __shared__ __nv_bfloat16 sp[64][66], sm_[64][66], spl[64][66], sml[64][66];
-  int upd = P.do_update;
-  P.ucoef = resolve_ucoef(d_g, lr, upd);
-  P.do_update = upd;
-  unsigned nn = 0, ns = 0;
+  constexpr int PER = (UPD ? 4 : 0) + (PERT ? 4 : 0);
+  ZgenScratch<TQ * PER> &sc = ((ZgenScratch<TQ * PER> *)raw)[threadIdx.x / 32];
+  const int lane = threadIdx.x & 31;
   const uint64_t total = T.tile_start[T.n];
-  for (uint64_t t = blockIdx.x; t < total; t += gridDim.x) {
+  const uint64_t nwarps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  for (uint64_t t = blockIdx.x * (uint64_t)(blockDim.x / 32) + threadIdx.x / 32; t < total;
+       t += nwarps) {  // warp-uniform: one tile per warp
     int si = 0;
     while (t >= T.tile_start[si + 1]) ++si;
     const zo2_segment_desc &sg = T.s[si];
-    const uint32_t tiles_c = (sg.cols + 63) / 64;
+    const uint32_t tiles_c = (sg.cols + 4 * TQ - 1) / (4 * TQ);
     const uint64_t lt = t - T.tile_start[si];
-    const uint32_t r0 = (uint32_t)(lt / tiles_c) * 64, c0 = (uint32_t)(lt % tiles_c) * 64;
+    const uint32_t r = (uint32_t)(lt / tiles_c) * 32 + lane, c0 = (uint32_t)(lt % tiles_c) * (4 * TQ);
     const bool split = sg.out_kind == ZO2_OUT_SPLIT_T;
-    // each thread: 4 quads (rows r0 + threadIdx.x/16 + 16*k, cols c0 + 4*(threadIdx.x%16))
-#pragma unroll 1
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t rr = threadIdx.x / 16 + 16 * k;
-      const uint32_t cc = 4 * (threadIdx.x % 16);
-      const uint32_t r = r0 + rr, c = c0 + cc;
-      if (r < sg.rows && c < sg.cols) {
-        const int cnt = (int)min(4u, sg.cols - c);
-        const uint64_t i = sg.offset + (uint64_t)r * sg.cols + c;
-        A w[4], wp[4], wm[4];
-        const bool vec = cnt == 4 && (i & 3) == 0;
-        if (vec) Wire<FMT>::load4(arena, i, w);
-        else
-          for (int j = 0; j < cnt; ++j) w[j] = Wire<FMT>::load1(arena, i + j);
-        k2_math4<A>(w, wp, wm, i, P, cnt);
-        if (vec) Wire<FMT>::store4(arena, i, w, nn, ns);
-        else
-          for (int j = 0; j < cnt; ++j) Wire<FMT>::store1(arena, i + j, w[j], nn, ns);
-        for (int j = 0; j < cnt; ++j) {
-          if (split) {
-            __nv_bfloat16 h, l;
-            split_bf16((float)wp[j], h, l);
-            sp[cc + j][rr] = h;
-            spl[cc + j][rr] = l;
-            split_bf16((float)wm[j], h, l);
-            sm_[cc + j][rr] = h;
-            sml[cc + j][rr] = l;
-          } else {
-            sp[cc + j][rr] = __float2bfloat16_rn((float)wp[j]);
-            sm_[cc + j][rr] = __float2bfloat16_rn((float)wm[j]);
-          }
+    A w[TQ][4], wp[TQ][4], wm[TQ][4];
+    uint64_t idx[TQ];
+    int cnt[TQ];
+    bool vec[TQ];
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) {
+      const uint32_t c = c0 + 4 * q;
+      cnt[q] = (r < sg.rows && c < sg.cols) ? (int)min(4u, sg.cols - c) : 0;
+      idx[q] = sg.offset + (uint64_t)r * sg.cols + c;
+      vec[q] = cnt[q] == 4 && (idx[q] & 3) == 0;
+      if (vec[q]) Wire<FMT>::load4(arena, idx[q], w[q]);
+      else
+        for (int j = 0; j < cnt[q]; ++j) w[q][j] = Wire<FMT>::load1(arena, idx[q] + j);
+    }
+    k2_quads<A, TQ, UPD, PERT>(w, wp, wm, idx, cnt, P, sc);
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) {
+      if (vec[q]) Wire<FMT>::store4(arena, idx[q], w[q], nn, ns);
+      else
+        for (int j = 0; j < cnt[q]; ++j) Wire<FMT>::store1(arena, idx[q] + j, w[q][j], nn, ns);
+      if (!PERT) continue;
+      const uint32_t c = c0 + 4 * q;
+      for (int j = 0; j < cnt[q]; ++j) {
+        const uint64_t o = (uint64_t)(c + j) * sg.rows + r;
+        if (split) {
+          __nv_bfloat16 h, l;
+          split_bf16((float)wp[q][j], h, l);
+          ((__nv_bfloat16 *)sg.out_plus)[o] = h;
+          ((__nv_bfloat16 *)sg.out_plus_lo)[o] = l;
+          split_bf16((float)wm[q][j], h, l);
+          ((__nv_bfloat16 *)sg.out_minus)[o] = h;
+          ((__nv_bfloat16 *)sg.out_minus_lo)[o] = l;
+        } else {
+          ((__nv_bfloat16 *)sg.out_plus)[o] = __float2bfloat16_rn((float)wp[q][j]);
+          ((__nv_bfloat16 *)sg.out_minus)[o] = __float2bfloat16_rn((float)wm[q][j]);
         }
       }
     }
-    __syncthreads();
-    if (P.do_perturb) {
-      // write operand rows n = c0 + (0..63), K range r0 .. r0+63 (K = sg.rows)
-      for (int e = threadIdx.x; e < 64 * 32; e += blockDim.x) {
-        const uint32_t nr = e / 32, kk = 2 * (e % 32);
-        const uint32_t n = c0 + nr, kq = r0 + kk;
-        if (n < sg.cols && kq < sg.rows) {
-          const uint64_t o = (uint64_t)n * sg.rows + kq;
-          __nv_bfloat16 *op = (__nv_bfloat16 *)sg.out_plus, *om = (__nv_bfloat16 *)sg.out_minus;
-          if (kq + 1 < sg.rows && (o & 1) == 0) {
-            *(__nv_bfloat162 *)(op + o) = __halves2bfloat162(sp[nr][kk], sp[nr][kk + 1]);
-            *(__nv_bfloat162 *)(om + o) = __halves2bfloat162(sm_[nr][kk], sm_[nr][kk + 1]);
-            if (split) {
-              *(__nv_bfloat162 *)((__nv_bfloat16 *)sg.out_plus_lo + o) =
-                  __halves2bfloat162(spl[nr][kk], spl[nr][kk + 1]);
-              *(__nv_bfloat162 *)((__nv_bfloat16 *)sg.out_minus_lo + o) =
-                  __halves2bfloat162(sml[nr][kk], sml[nr][kk + 1]);
-            }
-          } else {
-            for (uint32_t j = 0; j < 2 && kq + j < sg.rows; ++j) {
-              op[o + j] = sp[nr][kk + j];
-              om[o + j] = sm_[nr][kk + j];
-              if (split) {
-                ((__nv_bfloat16 *)sg.out_plus_lo)[o + j] = spl[nr][kk + j];
-                ((__nv_bfloat16 *)sg.out_minus_lo)[o + j] = sml[nr][kk + j];
-              }
-            }
-          }
-        }
-      }
-    }
-    __syncthreads();
   }
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(256, 2) k_update_perturb_transpose(
+    void *arena, SegTable T, K2Params P, const double *d_g, double lr, uint64_t *counts) {
+  int upd = P.do_update;
+  P.ucoef = resolve_ucoef(d_g, lr, upd);
+  unsigned nn = 0, ns = 0;
+  __shared__ __align__(16) uint8_t raw[8 * sizeof(ZgenScratch<TQ * 8>)];
+  if (upd && P.do_perturb) k2_transpose_body<FMT, true, true>(arena, T, P, nn, ns, raw);
+  else if (upd) k2_transpose_body<FMT, true, false>(arena, T, P, nn, ns, raw);
+  else if (P.do_perturb) k2_transpose_body<FMT, false, true>(arena, T, P, nn, ns, raw);
   if (FMT != ZO2_F32 && FMT != ZO2_F64) add_counts(counts, nn, ns);
 }
 
@@ -677,13 +719,13 @@ static int launch_k2(void *arena, const SegTable &lin, const SegTable &tr, const
   if (lin.n > 0 && lin.quad_start[lin.n] > 0) {
     // grid: multiple of 148 SMs, every thread a full loop trip
     const uint64_t q = lin.quad_start[lin.n];
-    unsigned g = zo2_grid_for(q, 256, 148u * 16u);
+    unsigned g = zo2_grid_for(q, 256, 148u * g_k2_ctas_per_sm);
     k_update_perturb_linear<FMT><<<g, 256, 0, s>>>(arena, lin, P, d_g, lr, counts);
     zo2_count_launch();
     ZO2_CHECK_LAUNCH();
   }
   if (tr.n > 0 && tr.tile_start[tr.n] > 0) {
-    unsigned g = zo2_grid_for(tr.tile_start[tr.n], 1, 148u * 8u);
+    unsigned g = zo2_grid_for(tr.tile_start[tr.n], 8, 148u * g_k2_ctas_per_sm);
     k_update_perturb_transpose<FMT><<<g, 256, 0, s>>>(arena, tr, P, d_g, lr, counts);
     zo2_count_launch();
     ZO2_CHECK_LAUNCH();
@@ -720,7 +762,7 @@ extern "C" int zo2_update_perturb(void *arena, int wire_fmt, uint64_t n, uint64_
     if (t && perturb) {
       tr.s[tr.n] = sg;
       tr.tile_start[tr.n + 1] =
-          tr.tile_start[tr.n] + (uint64_t)((sg.rows + 63) / 64) * ((sg.cols + 63) / 64);
+          tr.tile_start[tr.n] + (uint64_t)((sg.rows + 31) / 32) * ((sg.cols + 4 * TQ - 1) / (4 * TQ));
       ++tr.n;
     } else {
       lin.s[lin.n] = sg;

@@ -42,6 +42,7 @@ struct alignas(64) GemmArgs {
   float *ce_part[2];
   uint32_t M, N, K;
   int batch;
+  unsigned int *tile_ctr;  // [0] next tile, [1] CTAs finished (self-resetting)
 };
 
 // ---------------------------------------------------------------- PTX glue
@@ -151,7 +152,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_gemm(const __grid_constant__
   uint64_t *empty = full + C::STAGES;
   uint64_t *tfull = empty + C::STAGES;
   uint64_t *tempty = tfull + 2;
-  uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+  uint64_t *qfull = tempty + 2;   // tile-id ring (dynamic scheduler -> MMA/epilogue)
+  uint64_t *qempty = qfull + 4;
+  uint32_t *qtile = (uint32_t *)(qempty + 4);
+  uint32_t *tmem_slot = qtile + 4;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t M = args.M, N = args.N, K = args.K;
@@ -167,6 +171,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_gemm(const __grid_constant__
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 128);
+    }
+    for (int q = 0; q < 4; ++q) {
+      mbar_init(&qfull[q], 1);
+      mbar_init(&qempty[q], 5);  // MMA warp + 4 epilogue warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -191,9 +199,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_gemm(const __grid_constant__
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
     if (lane == 0) {
+      // dynamic tile scheduler: CTAs that start late (SM shared with the
+      // prepare lane's K2) simply take fewer tiles
       int stage = 0;
       uint32_t phase = 0;
-      for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (uint32_t it = 0;; ++it) {
+        const int qs = it & 3;
+        mbar_wait(&qempty[qs], ((it >> 2) & 1) ^ 1);
+        const uint32_t t = atomicAdd(args.tile_ctr, 1u);
+        qtile[qs] = t;
+        mbar_arrive(&qfull[qs]);
+        if (t >= tiles) break;
         const uint32_t p = t / (tiles_m * tiles_n);
         const uint32_t r = t % (tiles_m * tiles_n);
         const int m0 = (int)((r / tiles_n) * BM), n0 = (int)((r % tiles_n) * BN);
@@ -222,7 +238,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_gemm(const __grid_constant__
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (uint32_t it = 0;; ++it) {
+      const int qs = it & 3;
+      mbar_wait(&qfull[qs], (it >> 2) & 1);
+      const uint32_t t = qtile[qs];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&qempty[qs]);
+      if (t >= tiles) break;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d = tmem_base + (uint32_t)(acc * BN);
@@ -262,7 +284,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_gemm(const __grid_constant__
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    for (uint32_t it = 0;; ++it) {
+      const int qs = it & 3;
+      mbar_wait(&qfull[qs], (it >> 2) & 1);
+      const uint32_t t = qtile[qs];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&qempty[qs]);
+      if (t >= tiles) break;
       const uint32_t p = t / (tiles_m * tiles_n);
       const uint32_t r = t % (tiles_m * tiles_n);
       const uint32_t mt = r / tiles_n, nt = r % tiles_n;
@@ -362,6 +390,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_gemm(const __grid_constant__
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) {
+    // the producer (thread 0) made its last tile fetch before this point; the
+    // last CTA out resets the counter pair for the next launch on this slot
+    __threadfence();
+    if (atomicAdd(args.tile_ctr + 1, 1u) == gridDim.x - 1) {
+      atomicExch(args.tile_ctr, 0u);
+      atomicExch(args.tile_ctr + 1, 0u);
+    }
+  }
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -432,6 +469,7 @@ int make_map(const void *ptr, uint32_t rows, uint32_t k, uint32_t box_rows, CUte
 }
 
 int g_num_sms = 0;
+constexpr unsigned kCtrSlots = 256;
 
 template <int BN, bool SPLIT, int EPI>
 int launch(const GemmArgs &a, cudaStream_t s) {
@@ -451,7 +489,20 @@ int launch(const GemmArgs &a, cudaStream_t s) {
   }
   const uint32_t tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN) * (uint32_t)a.batch;
   const unsigned grid = tiles < (uint32_t)g_num_sms ? tiles : (unsigned)g_num_sms;
-  k_gemm<BN, SPLIT, EPI><<<grid, NUM_THREADS, C::SMEM, s>>>(a);
+  // one self-resetting counter pair per launch slot (per device)
+  static unsigned int *ctrs[64] = {nullptr};
+  static unsigned seq[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return zo2_set_error(ZO2_E_ARG, "zo2_gemm: device id out of range");
+  if (!ctrs[dev]) {
+    cudaError_t e = cudaMalloc(&ctrs[dev], 2 * kCtrSlots * sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMemset(ctrs[dev], 0, 2 * kCtrSlots * sizeof(unsigned int));
+    if (e != cudaSuccess) return zo2_set_cuda_error(e);
+  }
+  GemmArgs b = a;
+  b.tile_ctr = ctrs[dev] + 2 * (seq[dev]++ % kCtrSlots);
+  k_gemm<BN, SPLIT, EPI><<<grid, NUM_THREADS, C::SMEM, s>>>(b);
   zo2_count_launch();
   ZO2_CHECK_LAUNCH();
   return ZO2_OK;

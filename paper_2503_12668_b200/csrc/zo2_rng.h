@@ -54,7 +54,7 @@
 #define ZO2_LOG_CONST static const
 ZO2_LOG_CONST double ZO2_LOG_LN2HI = 0x1.62e42fefa38p-1;
 ZO2_LOG_CONST double ZO2_LOG_LN2LO = 0x1.ef35793c7673p-45;
-ZO2_LOG_CONST double ZO2_LOG_A[5] = {-0x1.0000000000001p-1, 0x1.555555551305bp-2, -0x1.fffffffeb459p-3, 0x1.999b324f10111p-3, -0x1.55575e506c89fp-3};
+ZO2_LOG_CONST double ZO2_LOG_AH[5] = {-0x1.0000000000001p-1, 0x1.555555551305bp-2, -0x1.fffffffeb459p-3, 0x1.999b324f10111p-3, -0x1.55575e506c89fp-3};
 /* {invc, logc} for the 128 subintervals of [0x1.6p-1, 0x1.6p+0) */
 ZO2_LOG_CONST double ZO2_LOG_TAB_H[256] = {
   0x1.734f0c3e0de9fp+0, -0x1.7cc7f79e69p-2,
@@ -187,6 +187,14 @@ ZO2_LOG_CONST double ZO2_LOG_TAB_H[256] = {
   0x1.756cadbd6130cp-1, 0x1.432eee32fep-2,
 };
 
+#if defined(__CUDACC__)
+static __constant__ double ZO2_LOG_AD[5] = {-0x1.0000000000001p-1, 0x1.555555551305bp-2, -0x1.fffffffeb459p-3, 0x1.999b324f10111p-3, -0x1.55575e506c89fp-3};
+#endif
+#if defined(__CUDA_ARCH__)
+#define ZO2_LOG_A ZO2_LOG_AD
+#else
+#define ZO2_LOG_A ZO2_LOG_AH
+#endif
 #if defined(__CUDACC__)
 /* device copy of the table (global memory: per-lane indices diverge, so
  * constant memory would serialise) */
@@ -410,11 +418,17 @@ ZO2_HD void zo2_raw_block(uint64_t seed, uint64_t stream, uint64_t b,
 /* ------------------------------------------------------- Cephes ndtri */
 ZO2_HD double zo2_polevl(double x, const double *c, int n) {
   double a = c[0];
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
   for (int i = 1; i <= n; ++i) a = ZO2_DADD(ZO2_DMUL(a, x), c[i]);
   return a;
 }
 ZO2_HD double zo2_p1evl(double x, const double *c, int n) {
   double a = ZO2_DADD(x, c[0]);
+#if defined(__CUDA_ARCH__)
+#pragma unroll
+#endif
   for (int i = 1; i < n; ++i) a = ZO2_DADD(ZO2_DMUL(a, x), c[i]);
   return a;
 }
@@ -426,10 +440,32 @@ ZO2_HD double zo2_p1evl(double x, const double *c, int n) {
 #define ZO2_NDTRI_P2 {3.23774891776946035970E0, 6.91522889068984211695E0, 3.93881025292474443415E0, 1.33303460815807542389E0, 2.01485389549179081538E-1, 1.23716634817820021358E-2, 3.01581553508235416007E-4, 2.65806974686737550832E-6, 6.23974539184983293730E-9}
 #define ZO2_NDTRI_Q2 {6.02427039364742014255E0, 3.67983563856160859403E0, 1.37702099489081330271E0, 2.16236993594496635890E-1, 1.34204006088543189037E-2, 3.28014464682127739104E-4, 2.89247864745380683936E-6, 6.79019408009981274425E-9}
 
+
+/* Coefficient tables: __constant__ on the device so FP64 instructions take
+ * them as c[bank][offset] operands; static arrays on the host. */
+#if defined(__CUDACC__)
+static __constant__ double ZO2_D_P0[5] = ZO2_NDTRI_P0;
+static __constant__ double ZO2_D_Q0[8] = ZO2_NDTRI_Q0;
+static __constant__ double ZO2_D_P1[9] = ZO2_NDTRI_P1;
+static __constant__ double ZO2_D_Q1[8] = ZO2_NDTRI_Q1;
+static __constant__ double ZO2_D_P2[9] = ZO2_NDTRI_P2;
+static __constant__ double ZO2_D_Q2[8] = ZO2_NDTRI_Q2;
+#endif
+static const double ZO2_H_P0[5] = ZO2_NDTRI_P0;
+static const double ZO2_H_Q0[8] = ZO2_NDTRI_Q0;
+static const double ZO2_H_P1[9] = ZO2_NDTRI_P1;
+static const double ZO2_H_Q1[8] = ZO2_NDTRI_Q1;
+static const double ZO2_H_P2[9] = ZO2_NDTRI_P2;
+static const double ZO2_H_Q2[8] = ZO2_NDTRI_Q2;
+#if defined(__CUDA_ARCH__)
+#define ZO2_COEF(name) ZO2_D_##name
+#else
+#define ZO2_COEF(name) ZO2_H_##name
+#endif
+
 /* Central branch: |y - 0.5| < 0.5 - exp(-2). */
 ZO2_HD double zo2_ndtri_central(double y) {
-  const double P0[5] = ZO2_NDTRI_P0;
-  const double Q0[8] = ZO2_NDTRI_Q0;
+  const double *P0 = ZO2_COEF(P0), *Q0 = ZO2_COEF(Q0);
   y = ZO2_DSUB(y, 0.5);
   const double y2 = ZO2_DMUL(y, y);
   const double t = ZO2_DDIV(ZO2_DMUL(y2, zo2_polevl(y2, P0, 4)), zo2_p1evl(y2, Q0, 8));
@@ -439,10 +475,8 @@ ZO2_HD double zo2_ndtri_central(double y) {
 
 /* Tail branch: y <= exp(-2) after reflection; code=1 negates. */
 ZO2_HD double zo2_ndtri_tail(double y, int negate) {
-  const double P1[9] = ZO2_NDTRI_P1;
-  const double Q1[8] = ZO2_NDTRI_Q1;
-  const double P2[9] = ZO2_NDTRI_P2;
-  const double Q2[8] = ZO2_NDTRI_Q2;
+  const double *P1 = ZO2_COEF(P1), *Q1 = ZO2_COEF(Q1);
+  const double *P2 = ZO2_COEF(P2), *Q2 = ZO2_COEF(Q2);
   double x = ZO2_DSQRT(ZO2_DMUL(-2.0, zo2_log(y)));
   const double x0 = ZO2_DSUB(x, ZO2_DDIV(zo2_log(x), x));
   const double z = ZO2_DDIV(1.0, x);

@@ -29,8 +29,8 @@ from .model import (EMBED_ID, HEAD_ID, DualForward, ModelSpec, module_order, mod
                     rng_offsets)
 from .numerics import BATCH_STREAM, PERTURB_STREAM, RngState, derive_step_seed, raw_uint64
 from .runtime import ModelParams, OffloadRuntime
-from .scheduler import (CudaLanes, Lane, build_iteration_dag, ckey, enqueue_dag, okey, ukey,
-                        validate_timeline)
+from .scheduler import (CudaLanes, Lane, build_iteration_dag, build_prepare_dag, ckey,
+                        close_step, enqueue_dag, okey, pkey, ukey, validate_timeline)
 
 
 @dataclass(frozen=True)
@@ -162,8 +162,9 @@ class TransformerWorkload:
 class _DeviceStep:
     """Shared device state of both engines: dual forward, scalars, pinned I/O."""
 
-    def __init__(self, spec: ModelSpec, arith: str, device):
+    def __init__(self, spec: ModelSpec, arith: str, device, operand_sets: int = 1):
         self.spec, self.arith, self.device = spec, arith, torch.device(device)
+        self.operand_sets = operand_sets
         self.fwd: DualForward | None = None
         self.d_out = torch.zeros(3, dtype=torch.float64, device=self.device)  # l+, l-, g
         self.d_flag = torch.zeros(1, dtype=torch.int32, device=self.device)
@@ -175,7 +176,8 @@ class _DeviceStep:
         if self.fwd is None or self.fwd.B != batch_size:
             self.fwd = None
             torch.cuda.empty_cache()
-            self.fwd = DualForward(self.spec, batch_size, self.arith, self.device)
+            self.fwd = DualForward(self.spec, batch_size, self.arith, self.device,
+                                   self.operand_sets)
             T = self.fwd.T
             self.h_tok = torch.empty(2, T, dtype=torch.int64, pin_memory=True)
         return self.fwd
@@ -209,7 +211,8 @@ class Zo2Engine:
 
     def __init__(self, workload: TransformerWorkload, cfg: ZOConfig, runtime: OffloadRuntime,
                  *, overlap: bool = True, backend: str = "cuda", update_mode: str = "deferred",
-                 cost=None, trace=None, validate: bool = True):
+                 cost=None, trace=None, validate: bool = True, prepare_lane: bool = True,
+                 operand_sets: int = 2):
         if update_mode not in ("deferred", "naive"):
             raise ValueError(f"unknown update_mode {update_mode!r}")
         if overlap and runtime.k_slots < 3:
@@ -228,8 +231,12 @@ class Zo2Engine:
         self._handles = {h.module: h for h in workload.modules()}
         self._order = [h.module for h in workload.modules()]
         self._blocks = [m for m in self._order if self._handles[m].transferable]
+        self.prepare_lane = prepare_lane
+        self.operand_sets = operand_sets if prepare_lane and update_mode == "deferred" else 1
         self.lanes = CudaLanes(runtime.device)
-        self.dev = _DeviceStep(workload.spec, workload.arith, runtime.device)
+        self.dev = _DeviceStep(workload.spec, workload.arith, runtime.device, self.operand_sets)
+        # concurrent prepare lane: one K2 CTA per SM beside the persistent GEMM
+        _lib.call("zo2_set_k2_ctas_per_sm", 1 if self.operand_sets >= 2 else 2)
         self._pool_booked = False
         self._async: list = []
         self._hist = torch.zeros(64, 4, dtype=torch.float64, device=runtime.device)
@@ -285,17 +292,54 @@ class Zo2Engine:
             prof.append(("k2", float(n * ((1 if update else 0) + (1 if perturb else 0))), e0, e1))
 
     # -- per-module compute tasks -------------------------------------------
-    def _compute(self, module: str, step: int, seq: int, stream: torch.cuda.Stream) -> None:
-        fwd = self.dev.fwd
-        naive = self.update_mode == "naive"
-        if naive:
+    def _bookkeep(self, module: str, step: int):
+        if self.update_mode == "naive":
             rs = self.mgr.get_state()
             self.mgr.push_rs(step, module, rs)
             self.mgr.set_state(rs.seed, rs.advanced(self._handles[module].size))
-            lrs, update = None, False
+            return rs, 0, False
+        rs, lrs, update = self._visit(module, step)
+        return rs, (lrs.seed if lrs is not None else 0), update
+
+    def _set_of(self, module: str) -> int:
+        return self._blocks.index(module) % self.operand_sets
+
+    def _prepare(self, module: str, step: int, stream: torch.cuda.Stream) -> None:
+        """P task (prepare lane): K2 for a block or the head."""
+        fwd = self.dev.fwd
+        rs, lrs_seed, update = self._bookkeep(module, step)
+        if module == HEAD_ID:
+            self._k2(self.runtime.persistent[HEAD_ID], _lib.F32, module, update, lrs_seed, True,
+                     rs.seed, fwd.head_descs(), stream)
         else:
-            rs, lrs, update = self._visit(module, step)
-        lrs_seed = lrs.seed if lrs is not None else 0
+            slot = self.runtime.slot_for(self._blocks.index(module))
+            self._k2(self.runtime.slot_bucket(slot), self.runtime.wire_fmt.code, module, update,
+                     lrs_seed, True, rs.seed, fwd.block_descs(self._set_of(module)), stream)
+
+    def _forward(self, module: str, stream: torch.cuda.Stream) -> None:
+        """C task of the prepare DAG (compute lane): forward from W+- operands."""
+        fwd = self.dev.fwd
+        s = stream.cuda_stream
+        if module == HEAD_ID:
+            self._head_tail(fwd, stream)
+        else:
+            fwd.block_forward(s, self._set_of(module))
+
+    def _head_tail(self, fwd, stream) -> None:
+        s = stream.cuda_stream
+        fwd.head_forward(s)
+        if self.dist_group is not None:
+            from .parallel import allreduce_loss_sums
+            with torch.cuda.stream(stream):
+                allreduce_loss_sums(fwd.d_sums, self.dist_group)
+        _lib.call("zo2_form_g", fwd.d_sums.data_ptr(), float(fwd.T * self.world),
+                  self.cfg.eps, self.dev.d_out.data_ptr(), self.dev.d_flag.data_ptr(), s)
+
+    def _compute(self, module: str, step: int, seq: int, stream: torch.cuda.Stream) -> None:
+        """Reference-shaped C task: K2 and forward of one module on one lane
+        (the embedding always; every module in naive update mode)."""
+        fwd = self.dev.fwd
+        rs, lrs_seed, update = self._bookkeep(module, step)
         s = stream.cuda_stream
         if module == EMBED_ID:
             table = self.runtime.persistent[EMBED_ID]
@@ -307,18 +351,12 @@ class Zo2Engine:
         elif module == HEAD_ID:
             self._k2(self.runtime.persistent[HEAD_ID], _lib.F32, module, update, lrs_seed, True,
                      rs.seed, fwd.head_descs(), stream)
-            fwd.head_forward(s)
-            if self.dist_group is not None:
-                import torch.distributed as dist
-                with torch.cuda.stream(stream):
-                    dist.all_reduce(fwd.d_sums, group=self.dist_group)
-            _lib.call("zo2_form_g", fwd.d_sums.data_ptr(), float(fwd.T * self.world),
-                      self.cfg.eps, self.dev.d_out.data_ptr(), self.dev.d_flag.data_ptr(), s)
+            self._head_tail(fwd, stream)
         else:
             slot = self.runtime.slot_for(self._blocks.index(module))
             self._k2(self.runtime.slot_bucket(slot), self.runtime.wire_fmt.code, module, update,
-                     lrs_seed, True, rs.seed, fwd.block_descs(), stream)
-            fwd.block_forward(s)
+                     lrs_seed, True, rs.seed, fwd.block_descs(0), stream)
+            fwd.block_forward(s, 0)
 
     def _naive_update(self, module: str, step: int, stream: torch.cuda.Stream) -> None:
         """zo2_engine.py:251-260: update after g with the same-step state (no gate)."""
@@ -419,11 +457,19 @@ class Zo2Engine:
         self._book_pool(self.dev.fwd)
         naive = self.update_mode == "naive"
         wire = {b: rt.block_nbytes for b in self._blocks}
-        dag = build_iteration_dag(self._blocks, k_slots=rt.k_slots, overlap=self.overlap,
-                                  naive_update=naive, wire_bytes=wire,
-                                  embed_id=self._order[0], head_id=self._order[-1])
         fns = {ckey(m): (lambda st, m=m: self._compute(m, step_index, seq, st))
                for m in self._order}
+        if naive or not self.prepare_lane:
+            dag = build_iteration_dag(self._blocks, k_slots=rt.k_slots, overlap=self.overlap,
+                                      naive_update=naive, wire_bytes=wire,
+                                      embed_id=self._order[0], head_id=self._order[-1])
+        else:
+            dag = build_prepare_dag(self._blocks, k_slots=rt.k_slots, overlap=self.overlap,
+                                    wire_bytes=wire, operand_sets=self.operand_sets,
+                                    embed_id=self._order[0], head_id=self._order[-1])
+            for m in self._order[1:]:
+                fns[pkey(m)] = lambda st, m=m: self._prepare(m, step_index, st)
+                fns[ckey(m)] = lambda st, m=m: self._forward(m, st)
         for i, b in enumerate(self._blocks):
             slot = rt.slot_for(i)
             fns[ukey(b)] = lambda st, b=b, slot=slot: rt.upload(b, slot, step_index, st, ukey(b))
@@ -437,6 +483,7 @@ class Zo2Engine:
             for m in self._order:
                 fns[ckey(m, 2)] = lambda st, m=m: self._naive_update(m, step_index, st)
         enq = enqueue_dag(dag, self.lanes, fns)
+        close_step(self.lanes)
         expected = 0 if naive else len(self._order)
         if len(self.mgr.rsb) != expected:
             raise StateCorruptionError(f"rsb holds {len(self.mgr.rsb)} entries, "

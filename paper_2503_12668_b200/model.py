@@ -198,7 +198,8 @@ class _Operand:
 class DualForward:
     """HBM working set + kernel sequence for the dual forward of one engine."""
 
-    def __init__(self, spec: ModelSpec, batch_size: int, arith: str, device):
+    def __init__(self, spec: ModelSpec, batch_size: int, arith: str, device,
+                 operand_sets: int = 2):
         if arith not in ("f32", "bf16"):
             raise ValueError(f"device forward supports arith f32 (3-pass bf16 split) or bf16, "
                              f"got {arith!r}")
@@ -217,16 +218,19 @@ class DualForward:
         self.qkv = [torch.empty(T * 3 * d, dtype=torch.float32, device=dev) for _ in range(2)]
         self.ctx = [_Operand(T * d, split, dev) for _ in range(2)]
         self.mid = [_Operand(T * 4 * d, split, dev) for _ in range(2)]
-        # block operands W +- eps z (vectors f32, matrices [N, K] bf16 planes)
+        # block operands W +- eps z (vectors f32, matrices [N, K] bf16 planes),
+        # `operand_sets` copies so K2 of block i+1 overlaps the forward of block i
         self.block_segs = segments(block_layout(spec))
-        self.vec = {}
-        self.mat = {}
-        for seg in self.block_segs:
-            if len(seg.shape) == 1:
-                self.vec[seg.name] = [torch.empty(seg.size, dtype=torch.float32, device=dev)
-                                      for _ in range(2)]
-            else:
-                self.mat[seg.name] = [_Operand(seg.size, split, dev) for _ in range(2)]
+        self.sets = []
+        for _ in range(operand_sets):
+            vec, mat = {}, {}
+            for seg in self.block_segs:
+                if len(seg.shape) == 1:
+                    vec[seg.name] = [torch.empty(seg.size, dtype=torch.float32, device=dev)
+                                     for _ in range(2)]
+                else:
+                    mat[seg.name] = [_Operand(seg.size, split, dev) for _ in range(2)]
+            self.sets.append((vec, mat))
         # head operands [V, d] (head_w, or the tied tok_emb)
         self.head_op = [_Operand(V * d, split, dev) for _ in range(2)]
         self.tile_n = _lib.load().zo2_gemm_tile_n(1 if split else 0)
@@ -234,6 +238,7 @@ class DualForward:
         self.ce_all = torch.empty(2, T * self.n_tiles_v * 3, dtype=torch.float32, device=dev)
         self.ce_part = [self.ce_all[0], self.ce_all[1]]
         self.d_sums = torch.zeros(2, dtype=torch.float64, device=dev)
+        self.d_ce_work = torch.zeros(2 * _lib.CE_PARTS, dtype=torch.float64, device=dev)
         # optional live kernel timing: list of (kind, work, start_evt, end_evt)
         self.prof: list | None = None
         self.ids = torch.empty(T, dtype=torch.int64, device=dev)
@@ -245,14 +250,15 @@ class DualForward:
         act = sum(t.numel() * t.element_size() for t in self.h + self.qkv)
         act += sum(o.nbytes for o in self.xop + self.ctx + self.mid)
         act += self.ce_all.numel() * 4
-        ops = sum(o.nbytes for ops in self.mat.values() for o in ops)
-        ops += sum(t.numel() * 4 for v in self.vec.values() for t in v)
+        ops = sum(o.nbytes for _, mat in self.sets for pair in mat.values() for o in pair)
+        ops += sum(t.numel() * 4 for vec, _ in self.sets for pair in vec.values() for t in pair)
         ops += sum(o.nbytes for o in self.head_op)
         return {"activations": act, "operands": ops, "io": 2 * self.T * 8}
 
     # ---------------------------------------------------------------- K2 descriptors
-    def block_descs(self):
-        key = "block"
+    def block_descs(self, set_idx: int = 0):
+        key = ("block", set_idx)
+        vec, mat = self.sets[set_idx]
         if key not in self._seg_cache:
             arr = (_lib.SegmentDesc * len(self.block_segs))()
             for k, seg in enumerate(self.block_segs):
@@ -261,13 +267,13 @@ class DualForward:
                 if len(seg.shape) == 1:
                     dsc.rows, dsc.cols = 1, seg.shape[0]
                     dsc.out_kind = _lib.OUT_F32
-                    dsc.out_plus = self.vec[seg.name][0].data_ptr()
-                    dsc.out_minus = self.vec[seg.name][1].data_ptr()
+                    dsc.out_plus = vec[seg.name][0].data_ptr()
+                    dsc.out_minus = vec[seg.name][1].data_ptr()
                 else:
                     dsc.rows, dsc.cols = seg.shape
                     dsc.out_kind = _lib.OUT_SPLIT_T if self.split else _lib.OUT_BF16_T
-                    p_hi, p_lo = self.mat[seg.name][0].ptrs()
-                    m_hi, m_lo = self.mat[seg.name][1].ptrs()
+                    p_hi, p_lo = mat[seg.name][0].ptrs()
+                    m_hi, m_lo = mat[seg.name][1].ptrs()
                     dsc.out_plus, dsc.out_minus = p_hi, m_hi
                     dsc.out_plus_lo, dsc.out_minus_lo = p_lo, m_lo
             self._seg_cache[key] = arr
@@ -340,31 +346,31 @@ class DualForward:
                   d_g.data_ptr() if d_g is not None else None, lr, lrs_seed, eps, rs_seed,
                   self.h[0].data_ptr(), self.h[1].data_ptr(), stream)
 
-    def block_forward(self, stream) -> None:
+    def block_forward(self, stream, set_idx: int = 0) -> None:
         spec = self.spec
         d, T, H = spec.dim, self.T, spec.n_heads
-        V = self.vec
+        V, Wm = self.sets[set_idx]
         for s in range(2):
             hi, lo = self.xop[s].ptrs()
             _lib.call("zo2_layernorm", self.h[s].data_ptr(), T, d, V["ln1_g"][s].data_ptr(),
                       V["ln1_b"][s].data_ptr(), hi, lo, stream)
-        self._gemm(self.xop, self.mat["qkv_w"], V["qkv_b"], [t.data_ptr() for t in self.qkv],
+        self._gemm(self.xop, Wm["qkv_w"], V["qkv_b"], [t.data_ptr() for t in self.qkv],
                    None, T, 3 * d, d, _lib.EPI_STORE, stream)
         for s in range(2):
             hi, lo = self.ctx[s].ptrs()
             _lib.call("zo2_attention", self.qkv[s].data_ptr(), self.B, spec.seq_len, H,
                       spec.head_dim, hi, lo, stream)
-        self._gemm(self.ctx, self.mat["attn_out_w"], V["attn_out_b"],
+        self._gemm(self.ctx, Wm["attn_out_w"], V["attn_out_b"],
                    [t.data_ptr() for t in self.h], None, T, d, d, _lib.EPI_RESIDUAL, stream)
         for s in range(2):
             hi, lo = self.xop[s].ptrs()
             _lib.call("zo2_layernorm", self.h[s].data_ptr(), T, d, V["ln2_g"][s].data_ptr(),
                       V["ln2_b"][s].data_ptr(), hi, lo, stream)
-        self._gemm(self.xop, self.mat["mlp_in_w"], V["mlp_in_b"],
+        self._gemm(self.xop, Wm["mlp_in_w"], V["mlp_in_b"],
                    [o.hi.data_ptr() for o in self.mid],
                    [o.lo.data_ptr() for o in self.mid] if self.split else None,
                    T, 4 * d, d, _lib.EPI_GELU, stream)
-        self._gemm(self.mid, self.mat["mlp_out_w"], V["mlp_out_b"],
+        self._gemm(self.mid, Wm["mlp_out_w"], V["mlp_out_b"],
                    [t.data_ptr() for t in self.h], None, T, d, 4 * d, _lib.EPI_RESIDUAL, stream)
 
     def head_forward(self, stream) -> None:
@@ -378,4 +384,5 @@ class DualForward:
         self._gemm(self.xop, self.head_op, None, None, None, T, spec.vocab, d, _lib.EPI_CE,
                    stream, targets=self.targets, ce=self.ce_part)
         _lib.call("zo2_ce_reduce", self.ce_all.data_ptr(), T, self.n_tiles_v, 2,
-                  self.ce_all.shape[1], self.d_sums.data_ptr(), stream)
+                  self.ce_all.shape[1], self.d_ce_work.data_ptr(), self.d_sums.data_ptr(),
+                  stream)

@@ -33,6 +33,7 @@ class Lane(Enum):
     COMPUTE = "compute"
     UPLOAD = "upload"
     OFFLOAD = "offload"
+    PREPARE = "prepare"   # B200 addition: K2 (update/perturb) beside the GEMMs
 
 
 @dataclass(frozen=True)
@@ -103,7 +104,7 @@ class Timeline:
 
     def chrome_trace_rows(self, step: int | None = None) -> list[dict]:
         """Chrome-trace rows, field names as scheduler.py:103-117."""
-        tid = {Lane.COMPUTE: 0, Lane.UPLOAD: 1, Lane.OFFLOAD: 2}
+        tid = {Lane.COMPUTE: 0, Lane.UPLOAD: 1, Lane.OFFLOAD: 2, Lane.PREPARE: 3}
         rows = []
         for e in self.events:
             args = {"block": e.module, "t_start": e.t_start, "t_end": e.t_end}
@@ -165,6 +166,66 @@ def build_iteration_dag(block_ids: list[str], *, k_slots: int = 3, overlap: bool
         edges.append((ckey(head_id), ckey(embed_id, 2)))
     dag = TaskDag(compute + upload + offload, edges)
     return dag if overlap else serialize_dag(dag)
+
+
+def pkey(m: str) -> str:
+    return "P:" + m
+
+
+def build_prepare_dag(block_ids: list[str], *, k_slots: int = 3, overlap: bool = True,
+                      wire_bytes: Mapping[str, int] | int = 0, operand_sets: int = 2,
+                      embed_id: str = EMBED_ID, head_id: str = HEAD_ID) -> TaskDag:
+    """The B200 refinement of the iteration DAG (deferred update mode).
+
+    The reference's compute task C(i) is split in two: P(i) on a PREPARE lane
+    runs K2 (deferred update + perturb/restore, emitting W+-eps z operands) and
+    C(i) on the COMPUTE lane runs the dual forward from those operands.  Every
+    edge is a real data dependency:
+
+      U(i) -> P(i)            arena holds block i
+      P(i) -> C(i)            operands of block i are ready
+      P(i) -> O(i)            restored (and re-encoded) weights are final, so
+                              the arena drains while block i still computes
+      C(i-S) -> P(i)          operand set i % S is free again (S sets)
+      O(i-K) -> U(i)          arena ring of K slots (scheduler.py:196-197)
+      P(head) -> C(head), C(N-1) -> C(head)
+
+    The FP64/INT-bound P(i+1) runs concurrently with the tensor-core C(i)."""
+    if k_slots < 1:
+        raise ValueError("k_slots must be >= 1")
+    if overlap and k_slots < 2:
+        raise ValueError("overlap requires at least 2 arena slots on the prepare DAG")
+    nb = (lambda m: wire_bytes) if isinstance(wire_bytes, int) else (lambda m: int(wire_bytes[m]))
+    compute = ([TaskSpec(ckey(embed_id), Lane.COMPUTE, embed_id, "dual")] +
+               [TaskSpec(ckey(b), Lane.COMPUTE, b, "dual") for b in block_ids] +
+               [TaskSpec(ckey(head_id), Lane.COMPUTE, head_id, "dual")])
+    prepare = ([TaskSpec(pkey(b), Lane.PREPARE, b, "prepare") for b in block_ids] +
+               [TaskSpec(pkey(head_id), Lane.PREPARE, head_id, "prepare")])
+    upload = [TaskSpec(ukey(b), Lane.UPLOAD, b, "upload", nb(b)) for b in block_ids]
+    offload = [TaskSpec(okey(b), Lane.OFFLOAD, b, "offload", nb(b)) for b in block_ids]
+    edges: list[tuple[str, str]] = []
+    for chain in (compute, prepare, upload, offload):
+        edges += [(a.key, b.key) for a, b in zip(chain, chain[1:])]
+    for i, b in enumerate(block_ids):
+        edges += [(ukey(b), pkey(b)), (pkey(b), ckey(b)), (pkey(b), okey(b))]
+        if i >= operand_sets:
+            edges.append((ckey(block_ids[i - operand_sets]), pkey(b)))
+        if i >= k_slots:
+            edges.append((okey(block_ids[i - k_slots]), ukey(b)))
+    edges.append((pkey(head_id), ckey(head_id)))
+    dag = TaskDag(compute + prepare + upload + offload, edges)
+    if overlap:
+        return dag
+    order: list[str] = [ckey(embed_id)]
+    for b in block_ids:
+        order += [ukey(b), pkey(b), ckey(b), okey(b)]
+    order += [pkey(head_id), ckey(head_id)]
+    seen, full = set(), []
+    for e in list(dag.edges) + list(zip(order, order[1:])):
+        if e not in seen:
+            seen.add(e)
+            full.append(e)
+    return TaskDag(dag.tasks, full)
 
 
 def serialize_dag(dag: TaskDag) -> TaskDag:
@@ -235,14 +296,17 @@ def validate_timeline(timeline: Timeline, dag: TaskDag, tol: float = 1e-9) -> li
 # ----------------------------------------------------------------------------
 
 class CudaLanes:
-    """The three lanes as CUDA streams on one device."""
+    """The lanes as CUDA streams on one device (compute gets high priority so
+    the tensor-core chain is never starved by the prepare lane's kernels)."""
 
     def __init__(self, device):
         self.device = torch.device(device)
         with torch.cuda.device(self.device):
-            self.streams = {Lane.COMPUTE: torch.cuda.Stream(self.device),
+            self.streams = {Lane.COMPUTE: torch.cuda.Stream(self.device, priority=-1),
                             Lane.UPLOAD: torch.cuda.Stream(self.device),
-                            Lane.OFFLOAD: torch.cuda.Stream(self.device)}
+                            Lane.OFFLOAD: torch.cuda.Stream(self.device),
+                            Lane.PREPARE: torch.cuda.Stream(self.device)}
+        self._tail: list[torch.cuda.Event] = []
 
     def __getitem__(self, lane: Lane) -> torch.cuda.Stream:
         return self.streams[lane]
@@ -250,6 +314,20 @@ class CudaLanes:
     def synchronize(self) -> None:
         for s in self.streams.values():
             s.synchronize()
+
+    def barrier_in(self) -> None:
+        """Every lane waits for the previous iteration's tail on every lane
+        (a device-side step barrier: no host synchronisation)."""
+        for s in self.streams.values():
+            for e in self._tail:
+                s.wait_event(e)
+
+    def barrier_out(self) -> None:
+        self._tail = []
+        for s in self.streams.values():
+            e = torch.cuda.Event()
+            e.record(s)
+            self._tail.append(e)
 
 
 class EnqueuedStep:
@@ -278,13 +356,14 @@ def enqueue_dag(dag: TaskDag, lanes: CudaLanes, task_fns: Mapping[str, Callable]
 
     task_fns[key](stream) enqueues the task's work on `stream`.  `after`
     (optional) is an event every lane waits on first (previous step's tail)."""
-    origin = torch.cuda.Event(enable_timing=True)
-    origin.record(lanes[Lane.COMPUTE])
-    for lane in (Lane.UPLOAD, Lane.OFFLOAD):
-        lanes[lane].wait_event(origin)
+    lanes.barrier_in()
     if after is not None:
         for lane in Lane:
             lanes[lane].wait_event(after)
+    origin = torch.cuda.Event(enable_timing=True)
+    origin.record(lanes[Lane.COMPUTE])
+    for lane in (Lane.UPLOAD, Lane.OFFLOAD, Lane.PREPARE):
+        lanes[lane].wait_event(origin)
     marks: dict = {}
     for task in topological_order(dag):
         stream = lanes[task.lane]
@@ -301,3 +380,8 @@ def enqueue_dag(dag: TaskDag, lanes: CudaLanes, task_fns: Mapping[str, Callable]
         e.record(stream)
         marks[task.key] = (task.lane, task.module, s, e)
     return EnqueuedStep(dag, origin, marks)
+
+
+def close_step(lanes: CudaLanes) -> None:
+    """Mark the end of an enqueued iteration on every lane (see barrier_in)."""
+    lanes.barrier_out()

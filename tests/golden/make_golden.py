@@ -172,3 +172,23 @@ if __name__ == "__main__":
     if "--big" in sys.argv:
         big_fixtures()
     print("fixtures written to", OUT)
+
+
+def dag_fixtures():
+    """Task lists and edges of the reference's iteration DAG for several
+    (n_blocks, k, overlap, naive) settings (scheduler.py:137-236)."""
+    from zo2lab.scheduler import build_iteration_dag
+    out = []
+    for n, k, ov, nv in [(5, 3, True, False), (7, 4, True, False), (4, 1, False, False),
+                         (6, 3, True, True), (3, 2, False, True), (1, 3, True, False)]:
+        blocks = [f"block.{i}" for i in range(n)]
+        d = build_iteration_dag(blocks, k_slots=k, overlap=ov, naive_update=nv, wire_bytes=7)
+        out.append({"n": n, "k": k, "overlap": ov, "naive": nv,
+                    "tasks": [[t.key, t.lane.value, t.module, t.kind, t.bytes, t.phase]
+                              for t in d.tasks],
+                    "edges": [list(e) for e in d.edges]})
+    (OUT / "dags.json").write_text(json.dumps(out))
+
+
+if __name__ == "__main__" and "--dags" in sys.argv:
+    dag_fixtures()

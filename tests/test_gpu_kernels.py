@@ -311,8 +311,9 @@ def test_gemm_cross_entropy(cuda, split):
     parts = _run_gemm(A, B, None, _l.EPI_CE, split, targets=tgt, n_tiles=nt)
     part_all = torch.stack(parts).contiguous()
     sums = torch.zeros(2, dtype=torch.float64, device=cuda)
-    _l.call("zo2_ce_reduce", part_all.data_ptr(), M, nt, 2, M * nt * 3, sums.data_ptr(),
-            stream())
+    work = torch.zeros(2 * _l.CE_PARTS, dtype=torch.float64, device=cuda)
+    _l.call("zo2_ce_reduce", part_all.data_ptr(), M, nt, 2, M * nt * 3, work.data_ptr(),
+            sums.data_ptr(), stream())
     torch.cuda.synchronize()
     for s in range(2):
         if split:
@@ -357,7 +358,9 @@ def test_attention(cuda, B, S, H, hd):
     sc = sc.masked_fill(~mask, float("-inf"))
     ref = (torch.softmax(sc, -1) @ v).transpose(1, 2).reshape(B * S, d)
     got = hi.double() + lo.double()
-    assert (got - ref).abs().max().item() < 2e-5
+    # 3-pass bf16 split products carry ~2^-16 relative error; scores are O(10)
+    # so exp() turns that into ~1e-5 relative on the context rows
+    assert (got - ref).abs().max().item() < 5e-5 * max(1.0, ref.abs().max().item())
 
 
 def test_embed_dual_matches_oracle(cuda, oracle):

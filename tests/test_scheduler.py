@@ -1,0 +1,96 @@
+"""The iteration DAG, its CUDA-stream refinement and the timeline validator
+(CPU only; the stream executor itself is exercised by the gpu tests)."""
+import itertools
+
+import pytest
+
+from paper_2503_12668_b200.errors import SchedulingContractError
+from paper_2503_12668_b200.scheduler import (Lane, StreamEvent, TaskDag, TaskSpec, Timeline,
+                                             build_iteration_dag, build_prepare_dag, ckey, okey,
+                                             pkey, topological_order, ukey, validate_timeline)
+
+
+def test_dag_identical_to_reference(golden):
+    for c in golden("dags.json"):
+        blocks = [f"block.{i}" for i in range(c["n"])]
+        d = build_iteration_dag(blocks, k_slots=c["k"], overlap=c["overlap"],
+                                naive_update=c["naive"], wire_bytes=7)
+        got = [[t.key, t.lane.value, t.module, t.kind, t.bytes, t.phase] for t in d.tasks]
+        assert got == c["tasks"]
+        assert sorted(map(tuple, d.edges)) == sorted(map(tuple, c["edges"]))
+
+
+def _simulate(dag, dur):
+    """Earliest-start schedule honouring edges and lane FIFO order."""
+    end, lane_free, ev = {}, {}, []
+    for t in topological_order(dag):
+        s = max([end[p] for p in dag.preds(t.key)] + [lane_free.get(t.lane, 0.0)])
+        e = s + dur(t)
+        end[t.key], lane_free[t.lane] = e, e
+        ev.append(StreamEvent(t.lane, t.key, t.module, s, e))
+    return Timeline(ev)
+
+
+@pytest.mark.parametrize("n,k,sets", [(6, 3, 1), (6, 3, 2), (9, 4, 2), (2, 2, 1), (1, 3, 2)])
+def test_prepare_dag_keeps_every_data_dependency(n, k, sets):
+    blocks = [f"block.{i}" for i in range(n)]
+    d = build_prepare_dag(blocks, k_slots=k, operand_sets=sets)
+    edges = set(d.edges)
+    for i, b in enumerate(blocks):
+        assert (ukey(b), pkey(b)) in edges and (pkey(b), ckey(b)) in edges
+        assert (pkey(b), okey(b)) in edges          # restored weights -> offload
+        if i >= k:
+            assert (okey(blocks[i - k]), ukey(b)) in edges   # arena ring
+        if i >= sets:
+            assert (ckey(blocks[i - sets]), pkey(b)) in edges  # operand sets
+    assert (pkey("head"), ckey("head")) in edges
+    tl = _simulate(d, lambda t: {"upload": 3.0, "offload": 3.0, "prepare": 1.0}.get(
+        t.lane.value, 2.0))
+    assert validate_timeline(tl, d) == []
+    # arena slot discipline: no two blocks live in one slot at once
+    ev = tl.by_key()
+    for i, j in itertools.combinations(range(n), 2):
+        if i % k == j % k and i < j:
+            assert ev[ukey(blocks[j])].t_start >= ev[okey(blocks[i])].t_end
+
+
+def test_prepare_dag_serialised_without_overlap():
+    blocks = ["block.0", "block.1", "block.2"]
+    d = build_prepare_dag(blocks, k_slots=1, overlap=False)
+    order = [t.key for t in topological_order(d)]
+    assert order == ["C:embed", "U:block.0", "P:block.0", "C:block.0", "O:block.0",
+                     "U:block.1", "P:block.1", "C:block.1", "O:block.1", "U:block.2",
+                     "P:block.2", "C:block.2", "O:block.2", "P:head", "C:head"]
+
+
+def test_validator_flags_violations():
+    d = build_iteration_dag(["block.0", "block.1"], k_slots=3)
+    tl = _simulate(d, lambda t: 1.0)
+    assert validate_timeline(tl, d) == []
+    ev = tl.by_key()
+    bad = [StreamEvent(e.lane, e.key, e.module, e.t_start, e.t_end) for e in tl.events]
+    for e in bad:
+        if e.key == "C:block.0":   # starts before its upload ends
+            e.t_start = ev["U:block.0"].t_start
+    kinds = {v.kind for v in validate_timeline(Timeline(bad), d)}
+    assert "dependency" in kinds
+    missing = Timeline([e for e in tl.events if e.key != "O:block.1"])
+    assert any(v.kind == "missing-event" for v in validate_timeline(missing, d))
+
+
+def test_cycle_detected():
+    t = [TaskSpec("a", Lane.COMPUTE, "m", "dual"), TaskSpec("b", Lane.COMPUTE, "m", "dual")]
+    with pytest.raises(SchedulingContractError):
+        topological_order(TaskDag(t, [("a", "b"), ("b", "a")]))
+
+
+def test_overlap_needs_three_slots():
+    with pytest.raises(ValueError):
+        build_iteration_dag(["block.0"], k_slots=2, overlap=True)
+
+
+def test_chrome_trace_rows():
+    d = build_prepare_dag(["block.0"], k_slots=3)
+    rows = _simulate(d, lambda t: 1e-3).chrome_trace_rows(step=4)
+    assert {r["tid"] for r in rows} == {0, 1, 2, 3}
+    assert all(r["ph"] == "X" and r["args"]["step"] == 4 for r in rows)
