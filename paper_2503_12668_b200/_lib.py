@@ -14,7 +14,7 @@ from .errors import (CapacityError, NonFiniteLossError, SchedulingContractError,
                      StateCorruptionError, UsageError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libzo2b200.so")
+LIB_PATH = os.environ.get("ZO2_LIB_PATH") or os.path.join(_HERE, "_lib", "libzo2b200.so")
 
 ZO2_OK, ZO2_E_ARG, ZO2_E_CUDA, ZO2_E_CAPACITY = 0, 1, 2, 3
 ZO2_E_SCHED, ZO2_E_STATE, ZO2_E_NONFINITE, ZO2_E_UNSUPPORTED = 4, 5, 6, 7

@@ -21,6 +21,7 @@ INCLUDE = PKG.parent / "include"
 
 SOURCES = ["zo2_elementwise.cu", "zo2_layers.cu", "zo2_gemm_sm100.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+EXTRA = os.environ.get("ZO2_NVCC_EXTRA", "").split()
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
          "-I", str(INCLUDE), "-I", str(CSRC)]
@@ -45,7 +46,7 @@ def _compile(src: str, verbose: bool) -> Path:
     s = CSRC / src
     o = LIBDIR / (s.stem + ".o")
     if _stale(o, _deps(s)):
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", str(s), "-o", str(o)]
+        cmd = [NVCC, *ARCH, *FLAGS, *EXTRA, "-c", str(s), "-o", str(o)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.run(cmd, check=True)

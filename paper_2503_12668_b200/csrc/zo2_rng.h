@@ -377,10 +377,23 @@ ZO2_HD double zo2_log(double x) {
 }
 
 /* ------------------------------------------------------------ Philox4x64 */
+#ifndef ZO2_MULHILO_EXPLICIT
+#define ZO2_MULHILO_EXPLICIT 0
+#endif
 ZO2_HD void zo2_mulhilo64(uint64_t a, uint64_t b, uint64_t *hi, uint64_t *lo) {
-#if defined(__CUDA_ARCH__)
+#if defined(__CUDA_ARCH__) && !ZO2_MULHILO_EXPLICIT
   *lo = a * b;
   *hi = __umul64hi(a, b);
+#elif defined(__CUDA_ARCH__)
+  // 128-bit product from four 32x32->64 multiply-adds (IMAD.WIDE.U32), the
+  // partial products shared between the high and the low half
+  const uint32_t al = (uint32_t)a, ah = (uint32_t)(a >> 32);
+  const uint32_t bl = (uint32_t)b, bh = (uint32_t)(b >> 32);
+  const uint64_t p0 = (uint64_t)al * bl;
+  const uint64_t t = (uint64_t)al * bh + (p0 >> 32);
+  const uint64_t u = (uint64_t)ah * bl + (uint32_t)t;
+  *lo = (u << 32) | (uint32_t)p0;
+  *hi = (uint64_t)ah * bh + (t >> 32) + (u >> 32);
 #else
   unsigned __int128 p = (unsigned __int128)a * b;
   *lo = (uint64_t)p;
@@ -457,15 +470,21 @@ static const double ZO2_H_P1[9] = ZO2_NDTRI_P1;
 static const double ZO2_H_Q1[8] = ZO2_NDTRI_Q1;
 static const double ZO2_H_P2[9] = ZO2_NDTRI_P2;
 static const double ZO2_H_Q2[8] = ZO2_NDTRI_Q2;
-#if defined(__CUDA_ARCH__)
-#define ZO2_COEF(name) ZO2_D_##name
+#ifndef ZO2_CONST_COEF
+#define ZO2_CONST_COEF 1
+#endif
+#if defined(__CUDA_ARCH__) && ZO2_CONST_COEF
+#define ZO2_DECL_COEF(var, name, n) const double *var = ZO2_D_##name;
+#elif defined(__CUDA_ARCH__)
+#define ZO2_DECL_COEF(var, name, n) const double var[n] = ZO2_NDTRI_##name;
 #else
-#define ZO2_COEF(name) ZO2_H_##name
+#define ZO2_DECL_COEF(var, name, n) const double *var = ZO2_H_##name;
 #endif
 
 /* Central branch: |y - 0.5| < 0.5 - exp(-2). */
 ZO2_HD double zo2_ndtri_central(double y) {
-  const double *P0 = ZO2_COEF(P0), *Q0 = ZO2_COEF(Q0);
+  ZO2_DECL_COEF(P0, P0, 5)
+  ZO2_DECL_COEF(Q0, Q0, 8)
   y = ZO2_DSUB(y, 0.5);
   const double y2 = ZO2_DMUL(y, y);
   const double t = ZO2_DDIV(ZO2_DMUL(y2, zo2_polevl(y2, P0, 4)), zo2_p1evl(y2, Q0, 8));
@@ -475,8 +494,10 @@ ZO2_HD double zo2_ndtri_central(double y) {
 
 /* Tail branch: y <= exp(-2) after reflection; code=1 negates. */
 ZO2_HD double zo2_ndtri_tail(double y, int negate) {
-  const double *P1 = ZO2_COEF(P1), *Q1 = ZO2_COEF(Q1);
-  const double *P2 = ZO2_COEF(P2), *Q2 = ZO2_COEF(Q2);
+  ZO2_DECL_COEF(P1, P1, 9)
+  ZO2_DECL_COEF(Q1, Q1, 8)
+  ZO2_DECL_COEF(P2, P2, 9)
+  ZO2_DECL_COEF(Q2, Q2, 8)
   double x = ZO2_DSQRT(ZO2_DMUL(-2.0, zo2_log(y)));
   const double x0 = ZO2_DSUB(x, ZO2_DDIV(zo2_log(x), x));
   const double z = ZO2_DDIV(1.0, x);

@@ -10,6 +10,9 @@
 // a given draw changes.
 #pragma once
 #include "zo2_rng.h"
+#ifndef ZO2_CENTRAL_BRANCHLESS
+#define ZO2_CENTRAL_BRANCHLESS 0
+#endif
 
 // Per-warp scratch: N*32 doubles (values / results) + N*32 queue entries.
 template <int N>
@@ -55,8 +58,13 @@ __device__ __forceinline__ void warp_ndtri(const double (&u)[N], double (&z)[N],
     const bool tail = !special && !(y > expm2);
     // central branch evaluated unconditionally (the warp executes it for
     // nearly every slot anyway): predication instead of a branch
+#if ZO2_CENTRAL_BRANCHLESS
     const double zc = zo2_ndtri_central(tail || special ? 0.5 : y);
     z[s] = special ? ((y0 == 1.0) ? INFINITY : -INFINITY) : zc;
+#else
+    if (special) z[s] = (y0 == 1.0) ? INFINITY : -INFINITY;
+    else if (!tail) z[s] = zo2_ndtri_central(y);
+#endif
     const unsigned m = __ballot_sync(0xffffffffu, tail);
     if (tail) {
       const unsigned pos = qn + __popc(m & lt);

@@ -511,7 +511,11 @@ class Zo2Engine:
                 if lrs is None:
                     raise StateCorruptionError(f"finalize: no lrs for {module}")
                 descs = self._update_descs(module)
-                if h.transferable:
+                if h.transferable and getattr(rt, "resident", False):
+                    # resident blocks (MeZO): the 'host master' is the device bucket
+                    self._k2(rt.host[module], rt.wire_fmt.code, module, 1, lrs.seed, False, 0,
+                             descs, comp)
+                elif h.transferable:
                     slot = 0
                     with torch.cuda.stream(comp):
                         rt.slots[slot].copy_(rt.host[module], non_blocking=True)
@@ -535,3 +539,52 @@ class Zo2Engine:
             self.step(dataset.batch(idx), j)
         self.finalize()
         return self.losses
+
+
+class MeZOEngine:
+    """All-resident MeZO engine, drop-in for zo_ref.RefEngine (zo_ref.py:82-121):
+    step(batch, j) -> g, .losses, .params, .train(dataset).
+
+    The arithmetic per parameter is the reference's (+eps, -2eps, +eps, then
+    -lr*g along the same z); the update is folded into the next step's fused
+    K2 pass exactly as the ZO2 engine does (SPEC C1: bit-identical result) and
+    is drained whenever .params is read, so the observable state after every
+    step equals RefEngine's."""
+
+    def __init__(self, workload: TransformerWorkload, cfg: ZOConfig, trace=None, *,
+                 device="cuda", capacity_bytes: float = float("inf")):
+        from .runtime import ResidentRuntime
+        self.workload, self.cfg, self.trace = workload, cfg, trace
+        self.runtime = ResidentRuntime(workload.params, capacity_bytes=capacity_bytes,
+                                       device=device)
+        k = self.runtime.k_slots
+        self._engine = Zo2Engine(workload, cfg, self.runtime, overlap=k >= 3, trace=trace)
+
+    @property
+    def losses(self) -> list[float]:
+        return self._engine.losses
+
+    @property
+    def gs(self) -> list[float]:
+        return self._engine.gs
+
+    @property
+    def timelines(self):
+        return self._engine.timelines
+
+    def step(self, batch, step_index: int) -> float:
+        return self._engine.step(batch, step_index)
+
+    @property
+    def params(self) -> ModelParams:
+        return self._engine.finalize()
+
+    def train(self, dataset, steps: int | None = None) -> list[float]:
+        steps = self.cfg.steps if steps is None else steps
+        for j in range(steps):
+            idx = batch_for_step(self.cfg.seed, j, dataset.n_samples, dataset.batch_size)
+            self.step(dataset.batch(idx), j)
+        return self.losses
+
+
+RefEngine = MeZOEngine

@@ -312,3 +312,48 @@ class OffloadRuntime:
                 "conversion": {"nan_count": self.conversion.nan_count,
                                "saturated_count": self.conversion.saturated_count},
                 "torch_max_allocated": int(torch.cuda.max_memory_allocated(self.device))}
+
+
+class ResidentRuntime(OffloadRuntime):
+    """All blocks resident in HBM (the MeZO / no-offload configuration, zo_ref.py):
+    one f32 device buffer per block serves as its permanent 'arena'; uploads and
+    offloads are no-ops, so the same engine and kernels run with zero host
+    traffic.  export_params() copies the device buckets back to the host view."""
+
+    resident = True
+
+    def __init__(self, params: ModelParams, *, capacity_bytes: float = float("inf"),
+                 device="cuda"):
+        self.params = params
+        self.spec = params.spec
+        self.codec = None
+        self.wire_fmt = params.fmt
+        self.device = torch.device(device)
+        self.pool = DevicePool(capacity_bytes)
+        self.log = TransferLog()
+        self.conversion = ConversionSummary()
+        self.current_step = 0
+        self._block_ids = [block_id(i) for i in range(self.spec.n_blocks)]
+        self.block_size = module_size(self.spec, block_id(0)) if self._block_ids else 0
+        self.k_slots = max(1, len(self._block_ids))
+        self.d_conv = torch.zeros(2, dtype=torch.int64, device=self.device)
+        self.persistent = {EMBED_ID: params.embedding, HEAD_ID: params.lm_head}
+        for t in self.persistent.values():
+            self.pool.alloc("persistent_params", t.numel() * 4)
+        self.pool.alloc("resident_blocks", len(self._block_ids) * self.block_nbytes)
+        self.slots = [b.to(self.device) for b in params.blocks]
+        self.host = {b: self.slots[i] for i, b in enumerate(self._block_ids)}
+        self._slot_owner = [None] * self.k_slots
+        self._pending_records = []
+
+    def upload(self, module, slot, step, stream, key=None) -> None:
+        pass
+
+    def offload(self, module, slot, step, stream, key=None) -> None:
+        pass
+
+    def export_params(self) -> ModelParams:
+        torch.cuda.synchronize(self.device)
+        for i, t in enumerate(self.slots):
+            self.params.blocks[i].copy_(t)
+        return self.params

@@ -190,5 +190,33 @@ def dag_fixtures():
     (OUT / "dags.json").write_text(json.dumps(out))
 
 
+def tied_fixtures():
+    """Tied LM head (model.py:145-148, :367-369): 6-step MeZO f32 run."""
+    spec = ModelSpec(2, 32, 4, 64, 16, tie_lm_head=True)
+    seed, T = 777, 6
+    cfg = ZOConfig(eps=1e-3, lr=1e-3, steps=T, seed=seed)
+    ds = gen_synthetic(64, 16, 32, N.RngState(seed), "affine", 2)
+    params = init_params(spec, N.RngState(seed), N.ElemFormat.F32)
+    ref = RefEngine(TransformerWorkload(params), cfg)
+    calls = []
+    orig = ref.workload.evaluate
+
+    def ev(batch, _o=orig, _c=calls):
+        v = _o(batch)
+        _c.append(v)
+        return v
+    ref.workload.evaluate = ev
+    for j in range(T):
+        ref.step(ds.batch(batch_for_step(seed, j, ds.n_samples, 2)), j)
+    lp, lm = calls[0::2], calls[1::2]
+    (OUT / "tied.json").write_text(json.dumps(
+        {"spec": [2, 32, 4, 64, 16], "seed": seed, "steps": T, "n_samples": 32,
+         "batch_size": 2, "eps": 1e-3, "lr": 1e-3, "l_plus": lp, "l_minus": lm,
+         "g": [(a - b) / 2e-3 for a, b in zip(lp, lm)], "digest": params_digest(params)}))
+    np.savez_compressed(OUT / "tied_final.npz", **{m: v for m, v in flat_params(params).items()})
+
+
 if __name__ == "__main__" and "--dags" in sys.argv:
     dag_fixtures()
+if __name__ == "__main__" and "--tied" in sys.argv:
+    tied_fixtures()
