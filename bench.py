@@ -217,7 +217,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     spec = ModelSpec(nb, d, H, V, S)
     B = cfg["B"]
     T = B * S
-    params = init_params(spec, RngState(SEED), device=dev)
+    # with a codec the blocks are encoded on device straight into pinned low-bit
+    # masters (no f32 host copy: OPT-30B f32 masters alone exceed host RAM)
+    params = init_params(spec, RngState(SEED), device=dev, codec=cfg["codec"])
     rt = OffloadRuntime(params, k_slots=cfg["slots"], codec=cfg["codec"],
                         capacity_bytes=cfg.get("cap", float("inf")), device=dev)
     eng = Zo2Engine(TransformerWorkload(params, cfg["arith"]),

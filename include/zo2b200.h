@@ -171,11 +171,13 @@ int zo2_to_operand(const float *x, uint64_t n, void *out_hi, void *out_lo,
  *   ZO2_EPI_GELU       C = gelu_erf(acc + bias) as an operand (bf16 / split)
  *   ZO2_EPI_CE         cross-entropy partials of the head logits per
  *                      (row, n-tile): max, sum exp, target logit  (model.py:304)
+ *   ZO2_EPI_OPERAND    C = acc + bias as bf16 (hi + lo) planes (qkv for attention)
  */
 #define ZO2_EPI_STORE 0
 #define ZO2_EPI_RESIDUAL 1
 #define ZO2_EPI_GELU 2
 #define ZO2_EPI_CE 3
+#define ZO2_EPI_OPERAND 4
 typedef struct zo2_gemm_problem {
   const void *a_hi, *a_lo;   /* [M, K] bf16                               */
   const void *b_hi, *b_lo;   /* [N, K] bf16                               */
@@ -199,11 +201,12 @@ int zo2_ce_reduce(const float *ce_part, uint32_t M, uint32_t n_tiles,
                   int batch, uint64_t part_stride, double *d_work,
                   double *d_sums, void *cuda_stream);
 
-/* model.py:273-283 causal softmax attention on packed qkv (f32 [B*S, 3d],
- * heads split as reshape(B,S,H,hd)), writing ctx as an A operand. */
-int zo2_attention(const float *qkv, uint32_t batch, uint32_t seq,
-                  uint32_t n_heads, uint32_t head_dim, void *ctx_hi,
-                  void *ctx_lo, void *cuda_stream);
+/* model.py:273-283 causal softmax attention on packed qkv given as bf16
+ * planes [B*S, 3d] (hi, and lo when split; heads split as reshape(B,S,H,hd)),
+ * writing ctx as an A operand (bf16 hi, + lo when split). */
+int zo2_attention(const void *qkv_hi, const void *qkv_lo, uint32_t batch,
+                  uint32_t seq, uint32_t n_heads, uint32_t head_dim,
+                  void *ctx_hi, void *ctx_lo, void *cuda_stream);
 
 #ifdef __cplusplus
 }

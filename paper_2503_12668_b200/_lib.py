@@ -22,7 +22,7 @@ ZO2_E_SCHED, ZO2_E_STATE, ZO2_E_NONFINITE, ZO2_E_UNSUPPORTED = 4, 5, 6, 7
 F64, F32, F16, BF16, F8E4M3 = 0, 1, 2, 3, 4
 
 OUT_NONE, OUT_F32, OUT_BF16_T, OUT_SPLIT_T, OUT_BF16, OUT_SPLIT = 0, 1, 2, 3, 4, 5
-EPI_STORE, EPI_RESIDUAL, EPI_GELU, EPI_CE = 0, 1, 2, 3
+EPI_STORE, EPI_RESIDUAL, EPI_GELU, EPI_CE, EPI_OPERAND = 0, 1, 2, 3, 4
 CE_PARTS = 148
 
 
@@ -71,7 +71,8 @@ _SIGS = {
     "zo2_gemm_tile_n": (c_int, [c_int]),
     "zo2_ce_reduce": (c_int, [c_void_p, c_uint32, c_uint32, c_int, c_uint64, c_void_p,
                               c_void_p, c_void_p]),
-    "zo2_attention": (c_int, [c_void_p, c_uint32, c_uint32, c_uint32, c_uint32, c_void_p,
+    "zo2_attention": (c_int, [c_void_p, c_void_p, c_uint32, c_uint32, c_uint32, c_uint32,
+                              c_void_p,
                               c_void_p, c_void_p]),
 }
 

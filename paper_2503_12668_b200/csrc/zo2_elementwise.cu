@@ -486,6 +486,47 @@ __device__ __forceinline__ void k2_quads(A (&w)[NQ][4], A (&wp)[NQ][4], A (&wm)[
                                          ZgenScratch<NQ *((UPD ? 4 : 0) + (PERT ? 4 : 0))> &sc) {
   constexpr int PER = (UPD ? 4 : 0) + (PERT ? 4 : 0);
   constexpr int OFF = UPD ? 4 : 0;
+#if ZO2_K2_TWO_PHASE
+  if (UPD && PERT) {
+    // two warp-cooperative passes of 4 draws per quad (update, then perturb):
+    // half the live f64 state, more resident warps
+    ZgenScratch<NQ * 4> &s4 = *reinterpret_cast<ZgenScratch<NQ * 4> *>(&sc);
+    double u[NQ * 4], z[NQ * 4];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      uint64_t r[4];
+      if (cnt[q] > 0) zo2_raw4(P.lrs_seed, ZO2_PERTURB_STREAM, P.base + idx[q], r);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) u[q * 4 + j] = j < cnt[q] ? zo2_u53(r[j]) : 0.5;
+    }
+    warp_ndtri<NQ * 4>(u, z, s4);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < cnt[q]) w[q][j] = axpy1(w[q][j], P.ucoef, z[q * 4 + j]);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      uint64_t r[4];
+      if (cnt[q] > 0) zo2_raw4(P.rs_seed, ZO2_PERTURB_STREAM, P.base + idx[q], r);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) u[q * 4 + j] = j < cnt[q] ? zo2_u53(r[j]) : 0.5;
+    }
+    warp_ndtri<NQ * 4>(u, z, s4);
+    const double m2 = -2.0 * P.eps;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j >= cnt[q]) continue;
+        const double zr = z[q * 4 + j];
+        wp[q][j] = axpy1(w[q][j], P.eps, zr);
+        wm[q][j] = axpy1(wp[q][j], m2, zr);
+        w[q][j] = axpy1(wm[q][j], P.eps, zr);
+      }
+    return;
+  }
+#endif
   double u[NQ * PER], z[NQ * PER];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
@@ -561,6 +602,12 @@ __device__ __forceinline__ void emit_linear(const zo2_segment_desc &sg, uint64_t
   }
 }
 
+#ifndef ZO2_K2_TWO_PHASE
+#define ZO2_K2_TWO_PHASE 0
+#endif
+#ifndef ZO2_K2_MINBLOCKS
+#define ZO2_K2_MINBLOCKS 2
+#endif
 #define ZO2_MAX_SEGS 16
 // quads (4 columns) per lane in the transposing K2: warp tile = 32 rows x 4*TQ cols
 constexpr int TQ = 1;
@@ -622,7 +669,7 @@ __device__ __forceinline__ void k2_linear_body(void *arena, const SegTable &T, c
 }
 
 template <int FMT>
-__global__ void __launch_bounds__(256, 2) k_update_perturb_linear(
+__global__ void __launch_bounds__(256, ZO2_K2_MINBLOCKS) k_update_perturb_linear(
     void *arena, SegTable T, K2Params P, const double *d_g, double lr, uint64_t *counts) {
   int upd = P.do_update;
   P.ucoef = resolve_ucoef(d_g, lr, upd);
@@ -701,7 +748,7 @@ __device__ __forceinline__ void k2_transpose_body(void *arena, const SegTable &T
 }
 
 template <int FMT>
-__global__ void __launch_bounds__(256, 2) k_update_perturb_transpose(
+__global__ void __launch_bounds__(256, ZO2_K2_MINBLOCKS) k_update_perturb_transpose(
     void *arena, SegTable T, K2Params P, const double *d_g, double lr, uint64_t *counts) {
   int upd = P.do_update;
   P.ucoef = resolve_ucoef(d_g, lr, upd);

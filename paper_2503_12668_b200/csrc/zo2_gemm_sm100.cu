@@ -350,14 +350,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_gemm(const __grid_constant__
                 for (int j = 0; j < 32 && col0 + j < N; ++j)
                   cp[j] = (EPI == ZO2_EPI_RESIDUAL) ? cp[j] + x[j] : x[j];
               }
-            } else {  // GELU -> bf16 operand planes
+            } else {  // GELU / OPERAND -> bf16 operand planes
               __nv_bfloat16 *hp = (__nv_bfloat16 *)args.c[p] + (uint64_t)row * N + col0;
               __nv_bfloat16 *lp =
                   SPLIT ? (__nv_bfloat16 *)args.c_lo[p] + (uint64_t)row * N + col0 : nullptr;
               __align__(16) __nv_bfloat16 hv[32], lv[32];
 #pragma unroll
               for (int j = 0; j < 32; ++j) {
-                const float g = gelu_erf(x[j]);
+                const float g = EPI == ZO2_EPI_GELU ? gelu_erf(x[j]) : x[j];
                 hv[j] = __float2bfloat16_rn(g);
                 lv[j] = __float2bfloat16_rn(g - __bfloat162float(hv[j]));
               }
@@ -515,6 +515,7 @@ int dispatch_epi(const GemmArgs &a, int epi, cudaStream_t s) {
     case ZO2_EPI_RESIDUAL: return launch<BN, SPLIT, ZO2_EPI_RESIDUAL>(a, s);
     case ZO2_EPI_GELU: return launch<BN, SPLIT, ZO2_EPI_GELU>(a, s);
     case ZO2_EPI_CE: return launch<BN, SPLIT, ZO2_EPI_CE>(a, s);
+    case ZO2_EPI_OPERAND: return launch<BN, SPLIT, ZO2_EPI_OPERAND>(a, s);
     default: return zo2_set_error(ZO2_E_ARG, "zo2_gemm: unknown epilogue");
   }
 }
@@ -554,7 +555,7 @@ extern "C" int zo2_gemm(const zo2_gemm_problem *probs, int batch, uint32_t M, ui
     if (epi == ZO2_EPI_CE && (!q.targets || !q.ce_part))
       return zo2_set_error(ZO2_E_ARG, "zo2_gemm: CE epilogue needs targets and ce_part");
     if (epi != ZO2_EPI_CE && !q.c) return zo2_set_error(ZO2_E_ARG, "zo2_gemm: null output");
-    if (epi == ZO2_EPI_GELU && split && !q.c_lo)
+    if ((epi == ZO2_EPI_GELU || epi == ZO2_EPI_OPERAND) && split && !q.c_lo)
       return zo2_set_error(ZO2_E_ARG, "zo2_gemm: split GELU needs c_lo");
   }
   cudaStream_t s = (cudaStream_t)cs;

@@ -175,338 +175,7 @@ extern "C" int zo2_to_operand(const float *x, uint64_t n, void *hi, void *lo, vo
   return ZO2_OK;
 }
 
-// ------------------------------------------------------------------ K5
-// SIMT flash attention (fp32): CTA = (query tile of 32, head, batch);
-// 8 lanes per query, each owning HD/8 dims of q and of the accumulator.
-template <int HD>
-__global__ void __launch_bounds__(256) k_attention(const float *qkv, uint32_t seq,
-                                                   uint32_t n_heads, __nv_bfloat16 *out_hi,
-                                                   __nv_bfloat16 *out_lo) {
-  constexpr int DPT = HD / 8;   // dims per thread
-  constexpr int KT = 32;        // keys per smem tile
-  __shared__ float ks[KT][HD + 4];
-  __shared__ float vs[KT][HD + 4];
-  const uint32_t dim = n_heads * HD;
-  const uint32_t ld = 3 * dim;
-  const uint32_t b = blockIdx.z, h = blockIdx.y;
-  const uint32_t q0 = blockIdx.x * 32;
-  const uint32_t qi = q0 + threadIdx.x / 8;
-  const uint32_t sub = threadIdx.x % 8;
-  const float scale = 1.0f / sqrtf((float)HD);
-  const float *base = qkv + (uint64_t)b * seq * ld;
-  float q[DPT], acc[DPT];
-  const bool valid = qi < seq;
-#pragma unroll
-  for (int j = 0; j < DPT; ++j) {
-    q[j] = valid ? base[(uint64_t)qi * ld + h * HD + sub * DPT + j] : 0.f;
-    acc[j] = 0.f;
-  }
-  float m = -INFINITY, l = 0.f;
-  const uint32_t kmax = min(seq, q0 + 32);  // causal: keys <= last query of tile
-  for (uint32_t k0 = 0; k0 < kmax; k0 += KT) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < KT * HD; e += 256) {
-      const int kr = e / HD, c = e % HD;
-      const uint32_t kk = k0 + kr;
-      ks[kr][c] = kk < seq ? base[(uint64_t)kk * ld + dim + h * HD + c] : 0.f;
-      vs[kr][c] = kk < seq ? base[(uint64_t)kk * ld + 2 * dim + h * HD + c] : 0.f;
-    }
-    __syncthreads();
-    const int kend = (int)min((uint32_t)KT, kmax - k0);
-    for (int kr = 0; kr < kend; ++kr) {
-      float sdot = 0.f;
-#pragma unroll
-      for (int j = 0; j < DPT; ++j) sdot += q[j] * ks[kr][sub * DPT + j];
-      sdot += __shfl_xor_sync(0xffffffffu, sdot, 1);
-      sdot += __shfl_xor_sync(0xffffffffu, sdot, 2);
-      sdot += __shfl_xor_sync(0xffffffffu, sdot, 4);
-      const uint32_t kk = k0 + kr;
-      if (valid && kk <= qi) {
-        const float sc = sdot * scale;
-        const float mn = fmaxf(m, sc);
-        const float corr = __expf(m - mn);
-        const float p = __expf(sc - mn);
-        l = l * corr + p;
-#pragma unroll
-        for (int j = 0; j < DPT; ++j) acc[j] = acc[j] * corr + p * vs[kr][sub * DPT + j];
-        m = mn;
-      }
-    }
-  }
-  if (valid) {
-    const float inv = 1.0f / l;
-    const uint64_t o = ((uint64_t)b * seq + qi) * dim + h * HD + sub * DPT;
-#pragma unroll
-    for (int j = 0; j < DPT; ++j) {
-      const float y = acc[j] * inv;
-      const __nv_bfloat16 hv = __float2bfloat16_rn(y);
-      out_hi[o + j] = hv;
-      if (out_lo) out_lo[o + j] = __float2bfloat16_rn(y - __bfloat162float(hv));
-    }
-  }
-}
-
-// Tensor-core flash attention (mma.sync m16n8k16 bf16 -> f32).  CTA = 64
-// queries (4 warps x 16 rows) of one (batch, head); key tiles of 64 up to the
-// causal diagonal; online softmax in f32 registers; P stays in registers as
-// the A operand of P.V.  SPLIT (f32 arithmetic): Q, K, V and P carry bf16
-// hi + lo parts and each product is hi.hi + hi.lo + lo.hi (~2^-16 relative).
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-  const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
-  return *reinterpret_cast<const uint32_t *>(&v);
-}
-__device__ __forceinline__ void split2(float a, float b, uint32_t &hi, uint32_t &lo) {
-  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-  hi = *reinterpret_cast<const uint32_t *>(&h);
-  lo = pack_bf16(a - __low2float(h), b - __high2float(h));
-}
-__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
-                                         uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-template <int HD, bool SPLIT>
-__global__ void __launch_bounds__(128) k_attn_mma(const float *qkv, uint32_t seq,
-                                                  uint32_t n_heads, __nv_bfloat16 *out_hi,
-                                                  __nv_bfloat16 *out_lo) {
-  constexpr int KB = 64, QB = 64;
-  constexpr int KP = HD + 8;  // padded row (bf16) for conflict-free 32-bit loads
-  constexpr int VP = KB + 8;
-  constexpr int NKS = HD / 16;     // k-steps of Q.K^T
-  constexpr int NOT = HD / 8;      // n-tiles of O
-  extern __shared__ __align__(16) uint8_t att_smem[];
-  __nv_bfloat16 *Kh = (__nv_bfloat16 *)att_smem;
-  __nv_bfloat16 *Kl = Kh + KB * KP;
-  __nv_bfloat16 *Vh = Kl + (SPLIT ? KB * KP : 0);   // transposed [HD][VP]
-  __nv_bfloat16 *Vl = Vh + HD * VP;
-
-  const uint32_t dim = n_heads * HD, ld = 3 * dim;
-  const uint32_t b = blockIdx.z, h = blockIdx.y;
-  const uint32_t n_qt = (seq + QB - 1) / QB;
-  const uint32_t qt = n_qt - 1 - blockIdx.x;  // heavy (late) tiles first
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int g = lane / 4, c = lane % 4;
-  const float *base = qkv + (uint64_t)b * seq * ld;
-  const uint32_t r0 = qt * QB + warp * 16 + g, r1 = r0 + 8;  // this thread's 2 rows
-  const float scale = 1.0f / sqrtf((float)HD);
-
-  // Q fragments (A operand, row-major 16 x 16 per k-step)
-  uint32_t qh[NKS][4], ql[NKS][4];
-#pragma unroll
-  for (int ks = 0; ks < NKS; ++ks) {
-#pragma unroll
-    for (int part = 0; part < 4; ++part) {
-      const uint32_t row = (part & 1) ? r1 : r0;
-      const int col = ks * 16 + (part >> 1) * 8 + 2 * c;
-      float x0 = 0.f, x1 = 0.f;
-      if (row < seq) {
-        const float2 v = *(const float2 *)(base + (uint64_t)row * ld + h * HD + col);
-        x0 = v.x;
-        x1 = v.y;
-      }
-      if (SPLIT) split2(x0, x1, qh[ks][part], ql[ks][part]);
-      else qh[ks][part] = pack_bf16(x0, x1);
-    }
-  }
-  float o[NOT][4];
-#pragma unroll
-  for (int i = 0; i < NOT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
-
-  const uint32_t k_end = min(seq, (qt + 1) * QB);
-  for (uint32_t k0 = 0; k0 < k_end; k0 += KB) {
-    __syncthreads();
-    // K tile [KB][HD] row-major, V tile transposed [HD][KB]
-    for (int e = threadIdx.x; e < KB * HD / 2; e += 128) {
-      const int kr = e / (HD / 2), cc = 2 * (e % (HD / 2));
-      const uint32_t key = k0 + kr;
-      float2 kv = make_float2(0.f, 0.f), vv = make_float2(0.f, 0.f);
-      if (key < seq) {
-        kv = *(const float2 *)(base + (uint64_t)key * ld + dim + h * HD + cc);
-        vv = *(const float2 *)(base + (uint64_t)key * ld + 2 * dim + h * HD + cc);
-      }
-      uint32_t kh, kl, vh2, vl2;
-      if (SPLIT) {
-        split2(kv.x, kv.y, kh, kl);
-        split2(vv.x, vv.y, vh2, vl2);
-        *(uint32_t *)(Kl + kr * KP + cc) = kl;
-        Vl[cc * VP + kr] = ((__nv_bfloat16 *)&vl2)[0];
-        Vl[(cc + 1) * VP + kr] = ((__nv_bfloat16 *)&vl2)[1];
-      } else {
-        kh = pack_bf16(kv.x, kv.y);
-        vh2 = pack_bf16(vv.x, vv.y);
-      }
-      *(uint32_t *)(Kh + kr * KP + cc) = kh;
-      Vh[cc * VP + kr] = ((__nv_bfloat16 *)&vh2)[0];
-      Vh[(cc + 1) * VP + kr] = ((__nv_bfloat16 *)&vh2)[1];
-    }
-    __syncthreads();
-    // S = Q K^T for this warp's 16 rows x 64 keys
-    float s[KB / 8][4];
-#pragma unroll
-    for (int nt = 0; nt < KB / 8; ++nt) {
-      s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-      const int kr = nt * 8 + g;
-#pragma unroll
-      for (int ks = 0; ks < NKS; ++ks) {
-        const uint32_t bh0 = *(const uint32_t *)(Kh + kr * KP + ks * 16 + 2 * c);
-        const uint32_t bh1 = *(const uint32_t *)(Kh + kr * KP + ks * 16 + 8 + 2 * c);
-        mma16816(s[nt], qh[ks], bh0, bh1);
-        if (SPLIT) {
-          const uint32_t bl0 = *(const uint32_t *)(Kl + kr * KP + ks * 16 + 2 * c);
-          const uint32_t bl1 = *(const uint32_t *)(Kl + kr * KP + ks * 16 + 8 + 2 * c);
-          mma16816(s[nt], qh[ks], bl0, bl1);
-          mma16816(s[nt], ql[ks], bh0, bh1);
-        }
-      }
-    }
-    // scale, causal / length mask, online softmax (rows r0 and r1)
-    float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-    for (int nt = 0; nt < KB / 8; ++nt) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint32_t key = k0 + nt * 8 + 2 * c + (j & 1);
-        const uint32_t row = (j < 2) ? r0 : r1;
-        float v = s[nt][j] * scale;
-        if (key > row || key >= seq) v = -INFINITY;
-        s[nt][j] = v;
-      }
-      mx0 = fmaxf(mx0, fmaxf(s[nt][0], s[nt][1]));
-      mx1 = fmaxf(mx1, fmaxf(s[nt][2], s[nt][3]));
-    }
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
-    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
-    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
-    const float n0 = fmaxf(m0, mx0), n1 = fmaxf(m1, mx1);
-    // rows with every key masked so far keep m = -inf; use 0 as the base
-    const float b0 = n0 == -INFINITY ? 0.f : n0, b1 = n1 == -INFINITY ? 0.f : n1;
-    const float cr0 = expf(m0 - b0), cr1 = expf(m1 - b1);
-    m0 = n0;
-    m1 = n1;
-    float ps0 = 0.f, ps1 = 0.f;
-#pragma unroll
-    for (int nt = 0; nt < KB / 8; ++nt) {
-      s[nt][0] = expf(s[nt][0] - b0);
-      s[nt][1] = expf(s[nt][1] - b0);
-      s[nt][2] = expf(s[nt][2] - b1);
-      s[nt][3] = expf(s[nt][3] - b1);
-      ps0 += s[nt][0] + s[nt][1];
-      ps1 += s[nt][2] + s[nt][3];
-    }
-    l0 = l0 * cr0 + ps0;
-    l1 = l1 * cr1 + ps1;
-#pragma unroll
-    for (int i = 0; i < NOT; ++i) {
-      o[i][0] *= cr0;
-      o[i][1] *= cr0;
-      o[i][2] *= cr1;
-      o[i][3] *= cr1;
-    }
-    // O += P V : P (registers) as A, V^T rows as B
-#pragma unroll
-    for (int kk = 0; kk < KB / 16; ++kk) {
-      uint32_t ph[4], pl[4];
-      if (SPLIT) {
-        split2(s[2 * kk][0], s[2 * kk][1], ph[0], pl[0]);
-        split2(s[2 * kk][2], s[2 * kk][3], ph[1], pl[1]);
-        split2(s[2 * kk + 1][0], s[2 * kk + 1][1], ph[2], pl[2]);
-        split2(s[2 * kk + 1][2], s[2 * kk + 1][3], ph[3], pl[3]);
-      } else {
-        ph[0] = pack_bf16(s[2 * kk][0], s[2 * kk][1]);
-        ph[1] = pack_bf16(s[2 * kk][2], s[2 * kk][3]);
-        ph[2] = pack_bf16(s[2 * kk + 1][0], s[2 * kk + 1][1]);
-        ph[3] = pack_bf16(s[2 * kk + 1][2], s[2 * kk + 1][3]);
-      }
-#pragma unroll
-      for (int nt = 0; nt < NOT; ++nt) {
-        const int vr = nt * 8 + g;
-        const uint32_t bh0 = *(const uint32_t *)(Vh + vr * VP + kk * 16 + 2 * c);
-        const uint32_t bh1 = *(const uint32_t *)(Vh + vr * VP + kk * 16 + 8 + 2 * c);
-        mma16816(o[nt], ph, bh0, bh1);
-        if (SPLIT) {
-          const uint32_t bl0 = *(const uint32_t *)(Vl + vr * VP + kk * 16 + 2 * c);
-          const uint32_t bl1 = *(const uint32_t *)(Vl + vr * VP + kk * 16 + 8 + 2 * c);
-          mma16816(o[nt], ph, bl0, bl1);
-          mma16816(o[nt], pl, bh0, bh1);
-        }
-      }
-    }
-  }
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-  const float i0 = 1.0f / l0, i1 = 1.0f / l1;
-#pragma unroll
-  for (int nt = 0; nt < NOT; ++nt) {
-    const int col = h * HD + nt * 8 + 2 * c;
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      const uint32_t row = half ? r1 : r0;
-      if (row >= seq) continue;
-      const float a = o[nt][2 * half] * (half ? i1 : i0);
-      const float bb = o[nt][2 * half + 1] * (half ? i1 : i0);
-      const uint64_t off = ((uint64_t)b * seq + row) * dim + col;
-      uint32_t hv, lv;
-      split2(a, bb, hv, lv);
-      *(uint32_t *)(out_hi + off) = hv;
-      if (SPLIT) *(uint32_t *)(out_lo + off) = lv;
-    }
-  }
-}
-
-template <int HD, bool SPLIT>
-static int launch_attn(const float *qkv, uint32_t batch, uint32_t seq, uint32_t nh,
-                       __nv_bfloat16 *hi, __nv_bfloat16 *lo, cudaStream_t s) {
-  constexpr int KB = 64, KP = HD + 8, VP = KB + 8;
-  const int smem = (SPLIT ? 2 : 1) * (KB * KP + HD * VP) * 2;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_attn_mma<HD, SPLIT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return zo2_set_cuda_error(e);
-    attr = true;
-  }
-  dim3 grid((seq + 63) / 64, nh, batch);
-  k_attn_mma<HD, SPLIT><<<grid, 128, smem, s>>>(qkv, seq, nh, hi, lo);
-  return ZO2_OK;
-}
-
-extern "C" int zo2_attention(const float *qkv, uint32_t batch, uint32_t seq, uint32_t n_heads,
-                             uint32_t head_dim, void *ctx_hi, void *ctx_lo, void *cs) {
-  if (batch == 0 || seq == 0) return ZO2_OK;
-  __nv_bfloat16 *hi = (__nv_bfloat16 *)ctx_hi, *lo = (__nv_bfloat16 *)ctx_lo;
-  const bool split = lo != nullptr;
-  cudaStream_t s = S(cs);
-  int rc = ZO2_OK;
-  switch (head_dim) {
-    case 16: rc = split ? launch_attn<16, true>(qkv, batch, seq, n_heads, hi, lo, s)
-                        : launch_attn<16, false>(qkv, batch, seq, n_heads, hi, lo, s); break;
-    case 32: rc = split ? launch_attn<32, true>(qkv, batch, seq, n_heads, hi, lo, s)
-                        : launch_attn<32, false>(qkv, batch, seq, n_heads, hi, lo, s); break;
-    case 64: rc = split ? launch_attn<64, true>(qkv, batch, seq, n_heads, hi, lo, s)
-                        : launch_attn<64, false>(qkv, batch, seq, n_heads, hi, lo, s); break;
-    case 128: rc = split ? launch_attn<128, true>(qkv, batch, seq, n_heads, hi, lo, s)
-                         : launch_attn<128, false>(qkv, batch, seq, n_heads, hi, lo, s); break;
-    case 8: {  // tiny heads (toy configs): SIMT path
-      dim3 grid((seq + 31) / 32, n_heads, batch);
-      k_attention<8><<<grid, 256, 0, s>>>(qkv, seq, n_heads, hi, lo);
-      break;
-    }
-    default:
-      return zo2_set_error(ZO2_E_UNSUPPORTED, "zo2_attention: head_dim not in {8,16,32,64,128}");
-  }
-  if (rc) return rc;
-  zo2_count_launch();
-  ZO2_CHECK_LAUNCH();
-  return ZO2_OK;
-}
+// K5 (attention) lives in zo2_attention.cu
 
 // ------------------------------------------------------------------ K7 tail
 // Combine per-(row, n-tile) partials {max, sum exp(x - max), target logit}

@@ -215,7 +215,7 @@ class DualForward:
         # residual streams and activations, one per sign
         self.h = [torch.empty(T * d, dtype=torch.float32, device=dev) for _ in range(2)]
         self.xop = [_Operand(T * d, split, dev) for _ in range(2)]
-        self.qkv = [torch.empty(T * 3 * d, dtype=torch.float32, device=dev) for _ in range(2)]
+        self.qkv = [_Operand(T * 3 * d, split, dev) for _ in range(2)]
         self.ctx = [_Operand(T * d, split, dev) for _ in range(2)]
         self.mid = [_Operand(T * 4 * d, split, dev) for _ in range(2)]
         # block operands W +- eps z (vectors f32, matrices [N, K] bf16 planes),
@@ -247,8 +247,8 @@ class DualForward:
 
     # ---------------------------------------------------------------- sizes
     def nbytes(self) -> dict[str, int]:
-        act = sum(t.numel() * t.element_size() for t in self.h + self.qkv)
-        act += sum(o.nbytes for o in self.xop + self.ctx + self.mid)
+        act = sum(t.numel() * t.element_size() for t in self.h)
+        act += sum(o.nbytes for o in self.xop + self.ctx + self.mid + self.qkv)
         act += self.ce_all.numel() * 4
         ops = sum(o.nbytes for _, mat in self.sets for pair in mat.values() for o in pair)
         ops += sum(t.numel() * 4 for vec, _ in self.sets for pair in vec.values() for t in pair)
@@ -354,12 +354,15 @@ class DualForward:
             hi, lo = self.xop[s].ptrs()
             _lib.call("zo2_layernorm", self.h[s].data_ptr(), T, d, V["ln1_g"][s].data_ptr(),
                       V["ln1_b"][s].data_ptr(), hi, lo, stream)
-        self._gemm(self.xop, Wm["qkv_w"], V["qkv_b"], [t.data_ptr() for t in self.qkv],
-                   None, T, 3 * d, d, _lib.EPI_STORE, stream)
+        # qkv = x @ W_qkv + b, emitted directly as the attention's bf16 planes
+        self._gemm(self.xop, Wm["qkv_w"], V["qkv_b"], [o.hi.data_ptr() for o in self.qkv],
+                   [o.lo.data_ptr() for o in self.qkv] if self.split else None,
+                   T, 3 * d, d, _lib.EPI_OPERAND, stream)
         for s in range(2):
             hi, lo = self.ctx[s].ptrs()
-            _lib.call("zo2_attention", self.qkv[s].data_ptr(), self.B, spec.seq_len, H,
-                      spec.head_dim, hi, lo, stream)
+            qh, ql = self.qkv[s].ptrs()
+            _lib.call("zo2_attention", qh, ql, self.B, spec.seq_len, H, spec.head_dim, hi, lo,
+                      stream)
         self._gemm(self.ctx, Wm["attn_out_w"], V["attn_out_b"],
                    [t.data_ptr() for t in self.h], None, T, d, d, _lib.EPI_RESIDUAL, stream)
         for s in range(2):

@@ -119,6 +119,8 @@ class ModelParams:
                  lm_head: torch.Tensor, fmt: ElemFormat = ElemFormat.F32):
         self.spec, self.embedding, self.blocks, self.lm_head, self.fmt = (
             spec, embedding, blocks, lm_head, fmt)
+        self.block_codec: ElemFormat | None = None  # blocks already hold wire-format bits
+        self.init_conversion = None
 
     def buckets(self) -> list[tuple[str, torch.Tensor]]:
         return ([(EMBED_ID, self.embedding)] +
@@ -152,9 +154,14 @@ class ModelParams:
 
 
 def init_params(spec: ModelSpec, state: RngState, fmt: ElemFormat = ElemFormat.F32,
-                device="cuda", pin: bool = True) -> ModelParams:
+                device="cuda", pin: bool = True, codec: str | None = None) -> ModelParams:
     """model.py:198-224 on device: bit-identical buckets, blocks then moved to
-    pinned host memory (the offload tier)."""
+    pinned host memory (the offload tier).
+
+    With `codec`, each block is encoded on the device straight into its pinned
+    low-bit host master (exactly HostBlockStore's encode at construction,
+    runtime.py:154-162) so the f32 block copy never exists on the host --
+    required for OPT-30B/175B, whose f32 masters would not fit in host RAM."""
     if fmt is not ElemFormat.F32:
         raise ValueError("the B200 engine keeps parameters in f32 (arith f32 / bf16)")
     seed = state.seed
@@ -163,15 +170,29 @@ def init_params(spec: ModelSpec, state: RngState, fmt: ElemFormat = ElemFormat.F
     head = torch.empty(module_size(spec, HEAD_ID), dtype=torch.float32, device=device)
     if head.numel():
         init_module_(spec, HEAD_ID, seed, head)
+    cfmt = CODEC_FORMATS[codec] if codec not in (None, "none") else None
     blocks = []
-    scratch = torch.empty(module_size(spec, block_id(0)), dtype=torch.float32, device=device)
+    n = module_size(spec, block_id(0))
+    scratch = torch.empty(n, dtype=torch.float32, device=device)
+    conv = torch.zeros(2, dtype=torch.int64, device=device)
+    enc = torch.empty(n, dtype=_TORCH_STORAGE[cfmt], device=device) if cfmt else None
+    s = torch.cuda.current_stream().cuda_stream
     for i in range(spec.n_blocks):
         init_module_(spec, block_id(i), seed, scratch)
-        host = torch.empty(scratch.numel(), dtype=torch.float32, pin_memory=pin)
-        host.copy_(scratch)
+        if cfmt is None:
+            host = torch.empty(n, dtype=torch.float32, pin_memory=pin)
+            host.copy_(scratch)
+        else:
+            _lib.call("zo2_encode", scratch.data_ptr(), enc.data_ptr(), cfmt.code, n,
+                      conv.data_ptr(), s)
+            host = torch.empty(n, dtype=enc.dtype, pin_memory=pin)
+            host.copy_(enc)
         blocks.append(host)
     torch.cuda.synchronize()
-    return ModelParams(spec, emb, blocks, head, fmt)
+    p = ModelParams(spec, emb, blocks, head, fmt)
+    p.block_codec = cfmt
+    p.init_conversion = conv
+    return p
 
 
 def params_digest(params) -> str:
@@ -211,9 +232,14 @@ class OffloadRuntime:
         sdt = _TORCH_STORAGE[self.wire_fmt]
         # host stores (HostBlockStore): alias the f32 masters, or encode them
         self.host: dict[str, torch.Tensor] = {}
-        if self.codec is None:
+        if params.block_codec is not None and params.block_codec is not self.codec:
+            raise ValueError(f"blocks were initialised as {params.block_codec.tag}, runtime "
+                             f"codec is {self.codec.tag if self.codec else 'none'}")
+        if self.codec is None or params.block_codec is self.codec:
             for i, b in enumerate(self._block_ids):
                 self.host[b] = params.blocks[i]
+            if params.init_conversion is not None:
+                self.d_conv += params.init_conversion
         else:
             scratch = torch.empty(self.block_size, dtype=torch.float32, device=self.device)
             enc = torch.empty(self.block_size, dtype=sdt, device=self.device)
@@ -296,11 +322,18 @@ class OffloadRuntime:
             scratch = torch.empty(self.block_size, dtype=torch.float32, device=self.device)
             enc = torch.empty(self.block_size, dtype=self.slots[0].dtype, device=self.device)
             s = torch.cuda.current_stream().cuda_stream
+            decoded = []
             for i, b in enumerate(self._block_ids):
                 enc.copy_(self.host[b])
                 _lib.call("zo2_decode", enc.data_ptr(), scratch.data_ptr(), self.codec.code,
                           self.block_size, s)
-                self.params.blocks[i].copy_(scratch)
+                if self.params.block_codec is None:
+                    self.params.blocks[i].copy_(scratch)
+                else:  # blocks alias the encoded masters: export into fresh f32 copies
+                    decoded.append(scratch.cpu())
+            if decoded:  # the runtime keeps its encoded masters in self.host
+                self.params.blocks = decoded
+                self.params.block_codec = None
             torch.cuda.synchronize()
         return self.params
 

@@ -19,7 +19,8 @@ pytestmark = pytest.mark.gpu
 LOSS_RTOL = 1e-5
 
 
-def _setup(golden, codec=None, arith="f32", k=3, overlap=True, mode="deferred"):
+def _setup(golden, codec=None, arith="f32", k=3, overlap=True, mode="deferred",
+           init_codec=False):
     from paper_2503_12668_b200.data import gen_synthetic
     from paper_2503_12668_b200.engine import (TransformerWorkload, ZOConfig, Zo2Engine,
                                               batch_for_step)
@@ -28,7 +29,7 @@ def _setup(golden, codec=None, arith="f32", k=3, overlap=True, mode="deferred"):
     from paper_2503_12668_b200.runtime import OffloadRuntime, init_params
     G = golden("toy.json")
     spec = ModelSpec(*G["spec"])
-    params = init_params(spec, RngState(G["seed"]))
+    params = init_params(spec, RngState(G["seed"]), codec=codec if init_codec else None)
     rt = OffloadRuntime(params, k_slots=k, codec=codec)
     cfg = ZOConfig(G["eps"], G["lr"], G["steps"], G["seed"])
     eng = Zo2Engine(TransformerWorkload(params, arith), cfg, rt, overlap=overlap,
@@ -84,9 +85,10 @@ def test_toy_free_running_tracks_reference(cuda, golden):
     assert np.all(np.isfinite(eng.gs))
 
 
-@pytest.mark.parametrize("codec", ["bf16", "f16", "f8"])
-def test_toy_codec_teacher_forced_bit_exact(cuda, golden, codec):
-    G, eng, batches = _setup(golden, codec=codec)
+@pytest.mark.parametrize("codec,init_codec", [("bf16", False), ("f16", False), ("f8", False),
+                                              ("bf16", True), ("f8", True)])
+def test_toy_codec_teacher_forced_bit_exact(cuda, golden, codec, init_codec):
+    G, eng, batches = _setup(golden, codec=codec, init_codec=init_codec)
     R = G["runs"][f"{codec}codec"]
     for j, b in enumerate(batches):
         eng.step(b, j)
