@@ -213,6 +213,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    _lib.call("zo2_set_gemm_variant", args.gemm_variant)
     nb, d, H, V, S = cfg["spec"]
     spec = ModelSpec(nb, d, H, V, S)
     B = cfg["B"]
@@ -368,6 +369,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--operand-sets", type=int, default=1,
                     help="1: K2 of block i+1 after the forward of block i; 2: concurrent")
+    ap.add_argument("--gemm-variant", type=int, default=0,
+                    help="0 auto (CTA pair for large shapes), 1 single-CTA, 2 pair")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     world = int(os.environ.get("WORLD_SIZE", "1"))

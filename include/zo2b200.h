@@ -189,8 +189,12 @@ typedef struct zo2_gemm_problem {
 } zo2_gemm_problem;
 int zo2_gemm(const zo2_gemm_problem *probs, int batch, uint32_t M, uint32_t N,
              uint32_t K, int epilogue, void *cuda_stream);
-/* N-tile width the GEMM uses (CE partial count = ceil(N / tile)). */
+/* Column width of the CE partials (CE partial count = ceil(N / width)). */
 int zo2_gemm_tile_n(int split);
+/* Kernel choice: 0 auto (CTA-pair cta_group::2 256x256 tiles when M >= 256
+ * and N >= 256, else single-CTA 128-row tiles), 1 single-CTA only, 2 pair
+ * whenever legal.  For A/B measurements and tests. */
+int zo2_set_gemm_variant(int variant);
 
 /* Combine CE partials into per-problem token sums (f64): sums[b] =
  * sum_t (logsumexp_t - logit_t[target_t])  (model.py:304-313 numerator).

@@ -143,6 +143,108 @@ struct Cfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+// Cross-entropy partials are emitted per CE_W output columns whatever the
+// tile width, so the partial count ceil(N / CE_W) is kernel independent.
+constexpr int CE_W = 128;
+
+// Epilogue of one accumulator row segment: this thread owns output row `row`
+// and columns [n0, n0 + BN) held in TMEM at column offset tbase.
+template <int BN, bool SPLIT, int EPI>
+__device__ __forceinline__ void epilogue_tile(const GemmArgs &args, uint32_t p, uint32_t row,
+                                              uint32_t n0, uint32_t tbase) {
+  const uint32_t M = args.M, N = args.N;
+  float run_max = -INFINITY, run_sum = 0.f, tgt = -INFINITY;
+  int64_t target = -1;
+  if (EPI == ZO2_EPI_CE && row < M) target = args.targets[p][row];
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    uint32_t v[32];
+    tmem_ld32(tbase + (uint32_t)c0, v);  // warp-collective: every lane executes it
+    const uint32_t col0 = n0 + (uint32_t)c0;
+    if (row < M && col0 < N) {
+      if (EPI == ZO2_EPI_CE) {
+        float cm = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < N) cm = fmaxf(cm, __uint_as_float(v[j]));
+        const float nm = fmaxf(run_max, cm);
+        float s = run_sum * expf(run_max - nm);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < N) s += expf(__uint_as_float(v[j]) - nm);
+        run_sum = s;
+        run_max = nm;
+        if (target >= (int64_t)col0 && target < (int64_t)col0 + 32 && target < (int64_t)N) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if ((int64_t)col0 + j == target) tgt = __uint_as_float(v[j]);
+        }
+      } else {
+        const float *bias = args.bias[p];
+        float x[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          x[j] = __uint_as_float(v[j]);
+          if (bias && col0 + j < N) x[j] += bias[col0 + j];
+        }
+        const bool full_chunk = (col0 + 32 <= N) && (N % 4 == 0);
+        if (EPI == ZO2_EPI_STORE || EPI == ZO2_EPI_RESIDUAL) {
+          float *cp = (float *)args.c[p] + (uint64_t)row * N + col0;
+          if (full_chunk) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              float4 o = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
+              if (EPI == ZO2_EPI_RESIDUAL) {
+                const float4 h = *(const float4 *)(cp + j);
+                o.x += h.x; o.y += h.y; o.z += h.z; o.w += h.w;
+              }
+              *(float4 *)(cp + j) = o;
+            }
+          } else {
+            for (int j = 0; j < 32 && col0 + j < N; ++j)
+              cp[j] = (EPI == ZO2_EPI_RESIDUAL) ? cp[j] + x[j] : x[j];
+          }
+        } else {  // GELU / OPERAND -> bf16 operand planes
+          __nv_bfloat16 *hp = (__nv_bfloat16 *)args.c[p] + (uint64_t)row * N + col0;
+          __nv_bfloat16 *lp =
+              SPLIT ? (__nv_bfloat16 *)args.c_lo[p] + (uint64_t)row * N + col0 : nullptr;
+          __align__(16) __nv_bfloat16 hv[32], lv[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float g = EPI == ZO2_EPI_GELU ? gelu_erf(x[j]) : x[j];
+            hv[j] = __float2bfloat16_rn(g);
+            lv[j] = __float2bfloat16_rn(g - __bfloat162float(hv[j]));
+          }
+          if (full_chunk && (N % 8 == 0)) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              *(uint4 *)(hp + j) = *(const uint4 *)(hv + j);
+              if (SPLIT) *(uint4 *)(lp + j) = *(const uint4 *)(lv + j);
+            }
+          } else {
+            for (int j = 0; j < 32 && col0 + j < N; ++j) {
+              hp[j] = hv[j];
+              if (SPLIT) lp[j] = lv[j];
+            }
+          }
+        }
+      }
+    }
+    // end of a CE_W-column chunk that holds at least one valid column
+    if (EPI == ZO2_EPI_CE && ((c0 + 32) % CE_W == 0) && row < M &&
+        col0 + 32 - CE_W < N) {
+      const uint32_t n_ce = (N + CE_W - 1) / CE_W;
+      float *o = args.ce_part[p] + ((uint64_t)row * n_ce + (col0 / CE_W)) * 3;
+      o[0] = run_max;
+      o[1] = run_sum;
+      o[2] = tgt;
+      run_max = -INFINITY;
+      run_sum = 0.f;
+      tgt = -INFINITY;
+    }
+  }
+}
+
 template <int BN, bool SPLIT, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1) k_gemm(const __grid_constant__ GemmArgs args) {
   using C = Cfg<BN, SPLIT>;
@@ -299,90 +401,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_gemm(const __grid_constant__
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN);
-      float run_max = -INFINITY, run_sum = 0.f, tgt = -INFINITY;
-      int64_t target = -1;
-      if (EPI == ZO2_EPI_CE && row < M) target = args.targets[p][row];
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(tbase + (uint32_t)c0, v);
-        const uint32_t col0 = n0 + (uint32_t)c0;
-        if (row < M && col0 < N) {
-          if (EPI == ZO2_EPI_CE) {
-            float cm = -INFINITY;
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (col0 + j < N) cm = fmaxf(cm, __uint_as_float(v[j]));
-            const float nm = fmaxf(run_max, cm);
-            float s = run_sum * expf(run_max - nm);
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (col0 + j < N) s += expf(__uint_as_float(v[j]) - nm);
-            run_sum = s;
-            run_max = nm;
-            if (target >= (int64_t)col0 && target < (int64_t)col0 + 32 && target < (int64_t)N) {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if ((int64_t)col0 + j == target) tgt = __uint_as_float(v[j]);
-            }
-          } else {
-            const float *bias = args.bias[p];
-            float x[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              x[j] = __uint_as_float(v[j]);
-              if (bias && col0 + j < N) x[j] += bias[col0 + j];
-            }
-            const bool full_chunk = (col0 + 32 <= N) && (N % 4 == 0);
-            if (EPI == ZO2_EPI_STORE || EPI == ZO2_EPI_RESIDUAL) {
-              float *cp = (float *)args.c[p] + (uint64_t)row * N + col0;
-              if (full_chunk) {
-#pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                  float4 o = make_float4(x[j], x[j + 1], x[j + 2], x[j + 3]);
-                  if (EPI == ZO2_EPI_RESIDUAL) {
-                    const float4 h = *(const float4 *)(cp + j);
-                    o.x += h.x; o.y += h.y; o.z += h.z; o.w += h.w;
-                  }
-                  *(float4 *)(cp + j) = o;
-                }
-              } else {
-                for (int j = 0; j < 32 && col0 + j < N; ++j)
-                  cp[j] = (EPI == ZO2_EPI_RESIDUAL) ? cp[j] + x[j] : x[j];
-              }
-            } else {  // GELU / OPERAND -> bf16 operand planes
-              __nv_bfloat16 *hp = (__nv_bfloat16 *)args.c[p] + (uint64_t)row * N + col0;
-              __nv_bfloat16 *lp =
-                  SPLIT ? (__nv_bfloat16 *)args.c_lo[p] + (uint64_t)row * N + col0 : nullptr;
-              __align__(16) __nv_bfloat16 hv[32], lv[32];
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const float g = EPI == ZO2_EPI_GELU ? gelu_erf(x[j]) : x[j];
-                hv[j] = __float2bfloat16_rn(g);
-                lv[j] = __float2bfloat16_rn(g - __bfloat162float(hv[j]));
-              }
-              if (full_chunk && (N % 8 == 0)) {
-#pragma unroll
-                for (int j = 0; j < 32; j += 8) {
-                  *(uint4 *)(hp + j) = *(const uint4 *)(hv + j);
-                  if (SPLIT) *(uint4 *)(lp + j) = *(const uint4 *)(lv + j);
-                }
-              } else {
-                for (int j = 0; j < 32 && col0 + j < N; ++j) {
-                  hp[j] = hv[j];
-                  if (SPLIT) lp[j] = lv[j];
-                }
-              }
-            }
-          }
-        }
-      }
-      if (EPI == ZO2_EPI_CE && row < M) {
-        float *o = args.ce_part[p] + ((uint64_t)row * tiles_n + nt) * 3;
-        o[0] = run_max;
-        o[1] = run_sum;
-        o[2] = tgt;
-      }
+      epilogue_tile<BN, SPLIT, EPI>(args, p, row, n0, tbase);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       acc ^= 1;
@@ -402,6 +421,227 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_gemm(const __grid_constant__
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"((uint32_t)C::TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------- 2-SM variant
+// A CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2: each CTA stages its own 128 rows of A and 128
+// rows of B, the leader issues the MMAs for the pair and each CTA's TMEM holds
+// its 128 output rows.  Per SM this moves 32 KB of operands per 64-deep
+// k-block instead of 48 KB for the same MMA work, which is what lifts the
+// GEMM off the L2->SM bandwidth ceiling of the 1-CTA 128x256 tile.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void *dst, const CUtensorMap *tm, uint64_t *bar,
+                                                 int x, int y) {
+  // completion bytes go to the leader CTA's barrier (peer bit cleared)
+  const uint32_t mbar = smem_u32(bar) & 0xFEFFFFFFu;
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)tm), "r"(mbar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit2_mc(uint64_t *bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t *bar) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+__host__ __device__ constexpr uint32_t idesc_bf16_m256(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+
+template <bool SPLIT>
+struct Cfg2 {
+  static constexpr int BN = 256;          // pair tile N (each CTA stages BN/2 rows of B)
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = (BN / 2) * BK * 2;
+  static constexpr int STAGE_BYTES = (SPLIT ? 2 : 1) * (A_BYTES + B_BYTES);
+  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <bool SPLIT, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    k_gemm2(const __grid_constant__ GemmArgs args) {
+  using C = Cfg2<SPLIT>;
+  constexpr int BN = C::BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = (uint64_t *)(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t *empty = full + C::STAGES;
+  uint64_t *tfull = empty + C::STAGES;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const uint32_t M = args.M, N = args.N, K = args.K;
+  const uint32_t tiles_m = (M + 2 * BM - 1) / (2 * BM), tiles_n = (N + BN - 1) / BN;
+  const uint32_t tiles = tiles_m * tiles_n * (uint32_t)args.batch;
+  const uint32_t kblocks = (K + BK - 1) / BK;
+  const uint32_t cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps in each of the 2 CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    for (int p = 0; p < args.batch; ++p)
+      for (int j = 0; j < 4; ++j)
+        if (SPLIT || (j & 1) == 0)
+          asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&args.tm[p][j]) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"((uint32_t)C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer (both CTAs)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (uint32_t t = cid; t < tiles; t += ncl) {
+        const uint32_t p = t / (tiles_m * tiles_n);
+        const uint32_t r = t % (tiles_m * tiles_n);
+        const int m0 = (int)((r / tiles_n) * 2 * BM + rank * BM);
+        const int n0 = (int)((r % tiles_n) * BN + rank * (BN / 2));
+        for (uint32_t kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t *st = smem + stage * C::STAGE_BYTES;
+          if (leader) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+          const int kx = (int)(kb * BK);
+          tma_load_2d_pair(st, &args.tm[p][0], &full[stage], kx, m0);
+          tma_load_2d_pair(st + C::A_BYTES, &args.tm[p][2], &full[stage], kx, n0);
+          if (SPLIT) {
+            tma_load_2d_pair(st + C::A_BYTES + C::B_BYTES, &args.tm[p][1], &full[stage], kx, m0);
+            tma_load_2d_pair(st + 2 * C::A_BYTES + C::B_BYTES, &args.tm[p][3], &full[stage], kx,
+                             n0);
+          }
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer (leader CTA only)
+    if (leader) {
+      constexpr uint32_t idesc = idesc_bf16_m256(BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (uint32_t t = cid; t < tiles; t += ncl) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(acc * BN);
+        for (uint32_t kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
+            const uint32_t sb = sa + C::A_BYTES;
+            const uint32_t sal = sb + C::B_BYTES;
+            const uint32_t sbl = sal + C::A_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint32_t koff = (uint32_t)k * 32;
+              const uint64_t da = sw128_desc(sa + koff), db = sw128_desc(sb + koff);
+              tc_mma2(d, da, db, idesc, (kb | (uint32_t)k) != 0);
+              if (SPLIT) {
+                tc_mma2(d, da, sw128_desc(sbl + koff), idesc, 1u);
+                tc_mma2(d, sw128_desc(sal + koff), db, idesc, 1u);
+              }
+            }
+            tc_commit2_mc(&empty[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (lane == 0) tc_commit2_mc(&tfull[acc], 0x3);
+        __syncwarp();
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (both CTAs, own 128 rows)
+    const int quad = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (uint32_t t = cid; t < tiles; t += ncl) {
+      const uint32_t p = t / (tiles_m * tiles_n);
+      const uint32_t r = t % (tiles_m * tiles_n);
+      const uint32_t m0 = (r / tiles_n) * 2 * BM + rank * BM, n0 = (r % tiles_n) * BN;
+      const uint32_t row = m0 + quad * 32 + lane;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN);
+      epilogue_tile<BN, SPLIT, EPI>(args, p, row, n0, tbase);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"((uint32_t)C::TMEM_COLS)
                  : "memory");
   }
@@ -520,9 +760,57 @@ int dispatch_epi(const GemmArgs &a, int epi, cudaStream_t s) {
   }
 }
 
+template <bool SPLIT, int EPI>
+int launch2(const GemmArgs &a, cudaStream_t s) {
+  using C = Cfg2<SPLIT>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm2<SPLIT, EPI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return zo2_set_cuda_error(e);
+    attr_set = true;
+  }
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  const uint32_t tiles =
+      ((a.M + 2 * BM - 1) / (2 * BM)) * ((a.N + C::BN - 1) / C::BN) * (uint32_t)a.batch;
+  const uint32_t pairs = tiles < (uint32_t)(g_num_sms / 2) ? tiles : (uint32_t)(g_num_sms / 2);
+  k_gemm2<SPLIT, EPI><<<2 * pairs, NUM_THREADS, C::SMEM, s>>>(a);
+  zo2_count_launch();
+  ZO2_CHECK_LAUNCH();
+  return ZO2_OK;
+}
+
+template <bool SPLIT>
+int dispatch_epi2(const GemmArgs &a, int epi, cudaStream_t s) {
+  switch (epi) {
+    case ZO2_EPI_STORE: return launch2<SPLIT, ZO2_EPI_STORE>(a, s);
+    case ZO2_EPI_RESIDUAL: return launch2<SPLIT, ZO2_EPI_RESIDUAL>(a, s);
+    case ZO2_EPI_GELU: return launch2<SPLIT, ZO2_EPI_GELU>(a, s);
+    case ZO2_EPI_CE: return launch2<SPLIT, ZO2_EPI_CE>(a, s);
+    case ZO2_EPI_OPERAND: return launch2<SPLIT, ZO2_EPI_OPERAND>(a, s);
+    default: return zo2_set_error(ZO2_E_ARG, "zo2_gemm: unknown epilogue");
+  }
+}
+
+int g_variant = 0;  // 0 auto, 1 single-CTA only, 2 CTA pair whenever legal
+
 }  // namespace
 
-extern "C" int zo2_gemm_tile_n(int split) { return split ? 128 : 256; }
+extern "C" int zo2_gemm_tile_n(int split) {
+  (void)split;
+  return CE_W;  // CE partials are per CE_W columns for every kernel variant
+}
+
+extern "C" int zo2_set_gemm_variant(int v) {
+  if (v < 0 || v > 2) return zo2_set_error(ZO2_E_ARG, "zo2_set_gemm_variant: 0, 1 or 2");
+  g_variant = v;
+  return ZO2_OK;
+}
 
 extern "C" int zo2_gemm(const zo2_gemm_problem *probs, int batch, uint32_t M, uint32_t N,
                         uint32_t K, int epi, void *cs) {
@@ -530,7 +818,9 @@ extern "C" int zo2_gemm(const zo2_gemm_problem *probs, int batch, uint32_t M, ui
   if (M == 0 || N == 0) return ZO2_OK;
   if (K == 0 || K % 8 != 0) return zo2_set_error(ZO2_E_UNSUPPORTED, "zo2_gemm: K must be a positive multiple of 8");
   const bool split = probs[0].a_lo != nullptr;
-  const int BN = split ? 128 : 256;
+  // CTA pair (256 x 256 tiles) for production shapes; single CTA for small ones
+  const bool pair = g_variant != 1 && M >= 2 * BM && N >= 256;
+  const int BROWS = pair ? 128 : (split ? 128 : 256);  // B rows staged per CTA
   GemmArgs a;
   memset(&a, 0, sizeof(a));
   a.M = M;
@@ -543,9 +833,9 @@ extern "C" int zo2_gemm(const zo2_gemm_problem *probs, int batch, uint32_t M, ui
     if (split != (q.a_lo != nullptr) || split != (q.b_lo != nullptr))
       return zo2_set_error(ZO2_E_ARG, "zo2_gemm: split planes must be given for A and B together");
     int rc = make_map(q.a_hi, M, K, BM, &a.tm[p][0]);
-    if (!rc) rc = make_map(q.b_hi, N, K, (uint32_t)BN, &a.tm[p][2]);
+    if (!rc) rc = make_map(q.b_hi, N, K, (uint32_t)BROWS, &a.tm[p][2]);
     if (!rc && split) rc = make_map(q.a_lo, M, K, BM, &a.tm[p][1]);
-    if (!rc && split) rc = make_map(q.b_lo, N, K, (uint32_t)BN, &a.tm[p][3]);
+    if (!rc && split) rc = make_map(q.b_lo, N, K, (uint32_t)BROWS, &a.tm[p][3]);
     if (rc) return rc;
     a.bias[p] = q.bias;
     a.c[p] = q.c;
@@ -559,5 +849,6 @@ extern "C" int zo2_gemm(const zo2_gemm_problem *probs, int batch, uint32_t M, ui
       return zo2_set_error(ZO2_E_ARG, "zo2_gemm: split GELU needs c_lo");
   }
   cudaStream_t s = (cudaStream_t)cs;
+  if (pair) return split ? dispatch_epi2<true>(a, epi, s) : dispatch_epi2<false>(a, epi, s);
   return split ? dispatch_epi<128, true>(a, epi, s) : dispatch_epi<256, false>(a, epi, s);
 }

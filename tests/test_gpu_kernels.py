@@ -250,12 +250,21 @@ def _run_gemm(A, B, bias, epi, split, C=None, targets=None, n_tiles=None):
     return outs
 
 
-SHAPES = [(128, 256, 64), (32, 96, 32), (300, 520, 200), (1024, 768, 768), (2048, 3072, 1024)]
+SHAPES = [(128, 256, 64), (32, 96, 32), (300, 520, 200), (1024, 768, 768), (2048, 3072, 1024),
+          (512, 256, 8192)]
+
+
+@pytest.fixture(params=[1, 2], ids=["cta1", "cta_pair"])
+def gemm_variant(request):
+    """Run each GEMM test on both kernels: single-CTA and the cta_group::2 pair."""
+    L().call("zo2_set_gemm_variant", request.param)
+    yield request.param
+    L().call("zo2_set_gemm_variant", 0)
 
 
 @pytest.mark.parametrize("split", [False, True])
 @pytest.mark.parametrize("M,N,K", SHAPES)
-def test_gemm_store_bias(cuda, split, M, N, K):
+def test_gemm_store_bias(cuda, gemm_variant, split, M, N, K):
     torch.manual_seed(0)
     A = torch.randn(2, M, K, device=cuda)
     B = torch.randn(2, N, K, device=cuda) * 0.05
@@ -274,7 +283,7 @@ def test_gemm_store_bias(cuda, split, M, N, K):
 
 
 @pytest.mark.parametrize("split", [False, True])
-def test_gemm_residual_and_gelu(cuda, split):
+def test_gemm_residual_and_gelu(cuda, gemm_variant, split):
     torch.manual_seed(1)
     M, N, K = 384, 512, 256
     A = torch.randn(2, M, K, device=cuda)
@@ -299,7 +308,7 @@ def test_gemm_residual_and_gelu(cuda, split):
 
 
 @pytest.mark.parametrize("split", [False, True])
-def test_gemm_cross_entropy(cuda, split):
+def test_gemm_cross_entropy(cuda, gemm_variant, split):
     torch.manual_seed(2)
     _l = L()
     M, N, K = 256, 1000, 128
