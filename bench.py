@@ -211,7 +211,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     from paper_2503_12668_b200.runtime import OffloadRuntime, init_params
     from paper_2503_12668_b200.scheduler import Lane
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", local_rank % torch.cuda.device_count())
     torch.cuda.set_device(dev)
     _lib.call("zo2_set_gemm_variant", args.gemm_variant)
     nb, d, H, V, S = cfg["spec"]
@@ -260,7 +260,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     torch.cuda.synchronize()
     l0 = lib.zo2_launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local_rank) as clk:
+    with Clocks(dev.index) as clk:
         e0.record(comp)
         for k in range(args.steps):
             eng.step_async(j + k)
@@ -382,8 +382,15 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # NCCL over NVLink on a real multi-GPU node; ZO2_DIST_BACKEND=gloo lets
+        # several ranks share one GPU for functional tests of the DP path
+        backend = os.environ.get("ZO2_DIST_BACKEND", "nccl")
+        dev = torch.device("cuda", local_rank % torch.cuda.device_count())
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, cfg, rank, world, local_rank)
     finally:

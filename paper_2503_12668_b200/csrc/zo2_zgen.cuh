@@ -21,20 +21,35 @@ struct ZgenScratch {
   uint16_t q[N * 32];
 };
 
+#ifndef ZO2_RAW4_NOINLINE
+#define ZO2_RAW4_NOINLINE 1
+#endif
+// Positions not aligned to a Philox block (never on the hot path: segment
+// offsets are multiples of 4 when d % 4 == 0) -- kept out of line so the hot
+// loop's code stays small enough for the instruction cache.
+#if ZO2_RAW4_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+void zo2_raw4_unaligned(uint64_t seed, uint64_t stream, uint64_t pos, uint64_t *r) {
+  for (int j = 0; j < 4; ++j) {
+    uint64_t b[4];
+    zo2_raw_block(seed, stream, (pos + j) >> 2, b);
+    r[j] = b[(pos + j) & 3];
+  }
+}
+
 // Raw draws for positions pos..pos+3 of (seed, stream).
 __device__ __forceinline__ void zo2_raw4(uint64_t seed, uint64_t stream, uint64_t pos,
                                          uint64_t r[4]) {
-  if ((pos & 3) == 0) {
-    zo2_raw_block(seed, stream, pos >> 2, r);
-  } else {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      uint64_t b[4];
-      zo2_raw_block(seed, stream, (pos + j) >> 2, b);
-      r[j] = b[(pos + j) & 3];
-    }
-  }
+  if ((pos & 3) == 0) zo2_raw_block(seed, stream, pos >> 2, r);
+  else zo2_raw4_unaligned(seed, stream, pos, r);
 }
+
+#ifndef ZO2_CENTRAL_ROLLED
+#define ZO2_CENTRAL_ROLLED 0
+#endif
 
 // All 32 lanes of the warp must call this together (convergent).
 template <int N>
@@ -44,7 +59,8 @@ __device__ __forceinline__ void warp_ndtri(const double (&u)[N], double (&z)[N],
   const unsigned lane = threadIdx.x & 31u;
   const unsigned lt = (1u << lane) - 1u;
   unsigned qn = 0;
-  unsigned tail_bits = 0;  // slots of this lane that went to the queue
+  unsigned tail_bits = 0;     // slots of this lane that went to the tail queue
+  unsigned special_bits = 0;  // u == 0 or u == 1 (z = -inf / +inf)
 #pragma unroll
   for (int s = 0; s < N; ++s) {
     const double y0 = u[s];
@@ -56,24 +72,31 @@ __device__ __forceinline__ void warp_ndtri(const double (&u)[N], double (&z)[N],
     }
     const bool special = (y0 == 1.0) || (y0 == 0.0);
     const bool tail = !special && !(y > expm2);
-    // central branch evaluated unconditionally (the warp executes it for
-    // nearly every slot anyway): predication instead of a branch
-#if ZO2_CENTRAL_BRANCHLESS
-    const double zc = zo2_ndtri_central(tail || special ? 0.5 : y);
-    z[s] = special ? ((y0 == 1.0) ? INFINITY : -INFINITY) : zc;
-#else
-    if (special) z[s] = (y0 == 1.0) ? INFINITY : -INFINITY;
-    else if (!tail) z[s] = zo2_ndtri_central(y);
-#endif
+    if (special) special_bits |= 1u << s;
     const unsigned m = __ballot_sync(0xffffffffu, tail);
     if (tail) {
       const unsigned pos = qn + __popc(m & lt);
       sc.q[pos] = (uint16_t)((s * 32 + lane) | (neg ? 0x8000u : 0u));
-      sc.val[s * 32 + lane] = y;
       tail_bits |= 1u << s;
     }
     qn += __popc(m);
+#if ZO2_CENTRAL_ROLLED
+    sc.val[s * 32 + lane] = y;
+#else
+    if (special) z[s] = (y0 == 1.0) ? INFINITY : -INFINITY;
+    else if (!tail) z[s] = zo2_ndtri_central(y);
+    if (tail) sc.val[s * 32 + lane] = y;
+#endif
   }
+#if ZO2_CENTRAL_ROLLED
+  // central branch in a rolled loop over the staged values: one copy of the
+  // rational evaluation in the instruction stream instead of N
+#pragma unroll 1
+  for (int s = 0; s < N; ++s) {
+    if (((tail_bits | special_bits) >> s) & 1u) continue;
+    sc.val[s * 32 + lane] = zo2_ndtri_central(sc.val[s * 32 + lane]);
+  }
+#endif
   __syncwarp();
   for (unsigned base = 0; base < qn; base += 32) {
     const unsigned i = base + lane;
@@ -85,7 +108,13 @@ __device__ __forceinline__ void warp_ndtri(const double (&u)[N], double (&z)[N],
   }
   __syncwarp();
 #pragma unroll
-  for (int s = 0; s < N; ++s)
+  for (int s = 0; s < N; ++s) {
+#if ZO2_CENTRAL_ROLLED
+    z[s] = ((special_bits >> s) & 1u) ? ((u[s] == 1.0) ? INFINITY : -INFINITY)
+                                      : sc.val[s * 32 + lane];
+#else
     if (tail_bits & (1u << s)) z[s] = sc.val[s * 32 + lane];
+#endif
+  }
   __syncwarp();
 }
