@@ -1,0 +1,534 @@
+// zo2_k2.cu -- K2: fused deferred ZO-SGD update + SPSA perturbation of one
+// module bucket, emitting the W+eps z / W-eps z GEMM operands (sm_100a).
+//
+// Reference arithmetic (bit-exact): zo2_engine.py:183-204 dual_forward,
+// _update_flat :168-174, _perturb :161-166, model.py:227-233 axpy, with z from
+// numerics.py:161-182 (Philox4x64-10 + Cephes ndtri).  Per element:
+//   w  = st(w + (-(lr g)) z(lrs))                       (deferred update)
+//   w+ = st(w + eps z(rs)); w- = st(w+ - 2eps z(rs)); w = st(w- + eps z(rs))
+//
+// Design (why it looks like this).  The kernel is bound by issue slots of
+// the exact Gaussian transform, not by HBM: ~60 FP64 + ~45 integer
+// instructions per draw, two draws per parameter.  Evaluated per lane, a
+// warp executes both Cephes branches (central 73% / tail 27% of draws) for
+// every draw slot.  Here one CTA processes a 1024-element tile in four
+// phases, with all draws of the tile staged in shared memory:
+//   P1  load mapping: vector load of 4 weights per thread into a shared W
+//       tile; Philox blocks of both streams; each draw is classified and its
+//       slot pushed on a CTA-wide queue -- tail draws at the front, central
+//       draws at the back (warp-scanned offsets, one shared atomic per warp).
+//   P2  every warp takes 32 consecutive queue entries at a time: tail
+//       entries first, then central ones, so exactly one warp-chunk per tile
+//       mixes the two branches; nothing else diverges.
+//   P3  apply mapping (transposed for [K, N] weight segments, so the operand
+//       rows [N, K] are written as 8-byte-per-lane coalesced runs): update +
+//       perturb/restore chain from the staged z, outputs written, restored
+//       weights back into the W tile.
+//   P4  load mapping again: restored (re-encoded) weights to the arena.
+// The division / square root / Philox building blocks come from
+// zo2_zexact.cuh (same IEEE results, fewer instructions).
+#include "zo2_common.cuh"
+#include "zo2_wire.cuh"
+#include "zo2_zexact.cuh"
+#include <string.h>
+
+void zo2_count_launch(uint64_t n = 1);
+
+namespace {
+
+constexpr int NT = 256;          // threads per CTA
+constexpr int TE = 1024;         // elements per tile (32 x 32, or 1024 linear)
+constexpr int NSLOT = 8 * NT;    // draw slots per tile (update 4 + perturb 4 per thread)
+constexpr int WPITCH = 33;       // W tile row pitch (conflict-free transposed reads)
+constexpr int MAX_SEGS = 16;
+#ifndef ZO2_K2_MINB
+#define ZO2_K2_MINB 3  // 80 registers: no spills; 3 CTAs (24 warps) per SM
+#endif
+
+// 0 = grid from occupancy; n = at most n CTAs per SM (leave room for a
+// concurrently running persistent GEMM)
+unsigned g_k2_ctas_per_sm = 0;
+
+struct K2Table {
+  zo2_segment_desc s[MAX_SEGS];
+  uint64_t tile_start[MAX_SEGS + 1];
+  uint32_t tiles_c[MAX_SEGS];   // column tiles (transposed segments)
+  uint8_t transposed[MAX_SEGS];
+  int n;
+};
+
+struct K2Params {
+  uint64_t base;  // module RNG offset
+  int do_update;  // 0 none, 1 deferred (gated on g != 0), 2 ungated (naive)
+  double ucoef;   // -(lr * g), resolved on device
+  uint64_t lrs_seed;
+  int do_perturb;
+  double eps;
+  uint64_t rs_seed;
+};
+
+template <typename A>
+struct K2Smem {
+  double z[NSLOT];                  // y (reflected uniform) in P1, z after P2
+  double logtab[256];               // glibc log (invc, logc) table
+  double ccoef[13];                 // central-branch coefficients
+  A w[2][32 * WPITCH];              // weight tile, double-buffered across tiles
+  uint16_t q[NSLOT];                // tail slots from the front, central from the back
+  unsigned counts[2];               // packed (n_tail | n_central << 16), per buffer
+};
+
+// Swizzled z index of draw k of load-thread t: k*256 + 32a + (b ^ (a | (k&1)<<3))
+// with t = 32a + b.  Load-mapping accesses (fixed k, t = 32a + lane) and the
+// transposed apply mapping both hit every 8-byte bank pair exactly twice.
+__device__ __forceinline__ int zslot(int k, int t) {
+  const int a = t >> 5, b = t & 31;
+  return k * NT + (a << 5) + (b ^ (a | ((k & 1) << 3)));
+}
+
+__device__ __forceinline__ void split_bf16(float x, __nv_bfloat16 &hi, __nv_bfloat16 &lo) {
+  hi = __float2bfloat16_rn(x);
+  lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(__nv_bfloat16 a, __nv_bfloat16 b) {
+  return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
+}
+
+// Element chain without the per-op NaN checks (finite weights and z); the
+// caller re-runs axpy1's exact NaN semantics when an input is not finite.
+template <bool UPD, bool PERT>
+__device__ __forceinline__ void chain_fast(float &w, float &wp, float &wm, double uc, double zu,
+                                           double eps, double zp) {
+  double x = (double)w;
+  if (UPD) x = (double)__double2float_rn(__dadd_rn(x, __dmul_rn(uc, zu)));
+  if (PERT) {
+    const double ez = __dmul_rn(eps, zp);  // (-2 eps) z == -2 (eps z) exactly
+    const float p = __double2float_rn(__dadd_rn(x, ez));
+    const float m = __double2float_rn(__fma_rn(-2.0, ez, (double)p));
+    wp = p;
+    wm = m;
+    w = __double2float_rn(__dadd_rn((double)m, ez));
+  } else {
+    w = (float)x;
+    wp = wm = w;
+  }
+}
+template <bool UPD, bool PERT>
+__device__ __forceinline__ void chain_fast(double &w, double &wp, double &wm, double uc, double zu,
+                                           double eps, double zp) {
+  double x = w;
+  if (UPD) x = __dadd_rn(x, __dmul_rn(uc, zu));
+  if (PERT) {
+    const double ez = __dmul_rn(eps, zp);
+    wp = __dadd_rn(x, ez);
+    wm = __fma_rn(-2.0, ez, wp);
+    w = __dadd_rn(wm, ez);
+  } else {
+    w = x;
+    wp = wm = x;
+  }
+}
+template <typename A>
+struct Chain3 {
+  A w, wp, wm;
+};
+template <bool UPD, bool PERT, typename A>
+__device__ __noinline__ Chain3<A> chain_exact(A w, double uc, double zu, double eps, double zp) {
+  Chain3<A> c;
+  A x = w;
+  if (UPD) x = axpy1(x, uc, zu);
+  if (PERT) {
+    c.wp = axpy1(x, eps, zp);
+    c.wm = axpy1(c.wp, -2.0 * eps, zp);
+    x = axpy1(c.wm, eps, zp);
+  } else {
+    c.wp = c.wm = x;
+  }
+  c.w = x;
+  return c;
+}
+
+// Operand stores for 4 consecutive output elements starting at o (same kind
+// for the transposed and the linear layouts: the index already points into
+// the operand).
+template <typename A>
+__device__ __forceinline__ void emit4(const zo2_segment_desc &sg, int kind, uint64_t o,
+                                      const A (&wp)[4], const A (&wm)[4], int cnt) {
+  if (kind == ZO2_OUT_F32) {
+    if (cnt == 4 && (o & 3) == 0) {
+      *(float4 *)((float *)sg.out_plus + o) =
+          make_float4((float)wp[0], (float)wp[1], (float)wp[2], (float)wp[3]);
+      *(float4 *)((float *)sg.out_minus + o) =
+          make_float4((float)wm[0], (float)wm[1], (float)wm[2], (float)wm[3]);
+    } else {
+      for (int j = 0; j < cnt; ++j) {
+        ((float *)sg.out_plus)[o + j] = (float)wp[j];
+        ((float *)sg.out_minus)[o + j] = (float)wm[j];
+      }
+    }
+  } else if (kind == ZO2_OUT_BF16 || kind == ZO2_OUT_BF16_T) {
+    __nv_bfloat16 p[4], m[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      p[j] = __float2bfloat16_rn((float)wp[j]);
+      m[j] = __float2bfloat16_rn((float)wm[j]);
+    }
+    if (cnt == 4 && (o & 3) == 0) {
+      *(uint2 *)((__nv_bfloat16 *)sg.out_plus + o) = make_uint2(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]));
+      *(uint2 *)((__nv_bfloat16 *)sg.out_minus + o) = make_uint2(pack_bf16(m[0], m[1]), pack_bf16(m[2], m[3]));
+    } else {
+      for (int j = 0; j < cnt; ++j) {
+        ((__nv_bfloat16 *)sg.out_plus)[o + j] = p[j];
+        ((__nv_bfloat16 *)sg.out_minus)[o + j] = m[j];
+      }
+    }
+  } else if (kind == ZO2_OUT_SPLIT || kind == ZO2_OUT_SPLIT_T) {
+    __nv_bfloat16 ph[4], pl[4], mh[4], ml[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      split_bf16((float)wp[j], ph[j], pl[j]);
+      split_bf16((float)wm[j], mh[j], ml[j]);
+    }
+    if (cnt == 4 && (o & 3) == 0) {
+      *(uint2 *)((__nv_bfloat16 *)sg.out_plus + o) = make_uint2(pack_bf16(ph[0], ph[1]), pack_bf16(ph[2], ph[3]));
+      *(uint2 *)((__nv_bfloat16 *)sg.out_plus_lo + o) = make_uint2(pack_bf16(pl[0], pl[1]), pack_bf16(pl[2], pl[3]));
+      *(uint2 *)((__nv_bfloat16 *)sg.out_minus + o) = make_uint2(pack_bf16(mh[0], mh[1]), pack_bf16(mh[2], mh[3]));
+      *(uint2 *)((__nv_bfloat16 *)sg.out_minus_lo + o) = make_uint2(pack_bf16(ml[0], ml[1]), pack_bf16(ml[2], ml[3]));
+    } else {
+      for (int j = 0; j < cnt; ++j) {
+        ((__nv_bfloat16 *)sg.out_plus)[o + j] = ph[j];
+        ((__nv_bfloat16 *)sg.out_plus_lo)[o + j] = pl[j];
+        ((__nv_bfloat16 *)sg.out_minus)[o + j] = mh[j];
+        ((__nv_bfloat16 *)sg.out_minus_lo)[o + j] = ml[j];
+      }
+    }
+  }
+}
+
+template <int FMT, bool UPD, bool PERT>
+__device__ __forceinline__ void k2_tiles(void *arena, const K2Table &T, const K2Params &P,
+                                         K2Smem<typename Wire<FMT>::A> &sm, unsigned &nn,
+                                         unsigned &ns) {
+  typedef typename Wire<FMT>::A A;
+  constexpr int OFF = UPD ? 4 : 0;  // first perturb slot
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const double expm2 = 0.13533528323661269189;
+  const double one_m = __dsub_rn(1.0, expm2);
+  const uint64_t total = T.tile_start[T.n];
+  int buf = 0, si = 0;
+  for (uint64_t tile = blockIdx.x; tile < total; tile += gridDim.x, buf ^= 1) {
+    while (tile >= T.tile_start[si + 1]) ++si;  // tiles ascend: si never moves back
+    const zo2_segment_desc &sg = T.s[si];
+    const bool tr = T.transposed[si] != 0;
+    const uint64_t ltile = tile - T.tile_start[si];
+    A *W = sm.w[buf];
+
+    // ---------------- P1: load mapping
+    uint32_t r0 = 0, c0 = 0;
+    uint64_t e0 = 0, idx;
+    int cnt, widx;
+    if (tr) {
+      r0 = (uint32_t)(ltile / T.tiles_c[si]) * 32;
+      c0 = (uint32_t)(ltile % T.tiles_c[si]) * 32;
+      const uint32_t r = r0 + (t >> 3), c = c0 + 4 * (t & 7);
+      cnt = (r < sg.rows && c < sg.cols) ? (int)min(4u, sg.cols - c) : 0;
+      idx = sg.offset + (uint64_t)r * sg.cols + c;
+      widx = (t >> 3) * WPITCH + 4 * (t & 7);
+    } else {
+      e0 = ltile * TE;
+      const uint64_t seg_n = (uint64_t)sg.rows * sg.cols;
+      const uint64_t e = e0 + 4 * (uint64_t)t;
+      cnt = e < seg_n ? (int)min((uint64_t)4, seg_n - e) : 0;
+      idx = sg.offset + e;
+      widx = 4 * t;
+    }
+    A w[4] = {0, 0, 0, 0};
+    const bool vec = cnt == 4 && (idx & 3) == 0;
+    if (vec) Wire<FMT>::load4(arena, idx, w);
+    else
+      for (int j = 0; j < cnt; ++j) w[j] = Wire<FMT>::load1(arena, idx + j);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) W[widx + j] = w[j];
+
+    unsigned tmask = 0, cmask = 0, negmask = 0;
+    auto classify = [&](int k, uint64_t raw, bool valid) {
+      if (!valid) return;
+      const double u = zx_u53(raw);
+      double y = u;
+      bool neg = true;
+      if (y > one_m) {
+        y = __dsub_rn(1.0, y);
+        neg = false;
+      }
+      const int zi = zslot(k, t);
+      if (u == 1.0) {
+        sm.z[zi] = INFINITY;  // ndtri(1) = +inf (u > 0 always)
+      } else if (y > expm2) {
+        sm.z[zi] = y;
+        cmask |= 1u << k;
+      } else {
+        sm.z[zi] = y;
+        tmask |= 1u << k;
+        if (neg) negmask |= 1u << k;
+      }
+    };
+    if (cnt > 0) {
+      uint64_t r[4];
+      if (UPD) {
+        zx_raw4(P.lrs_seed, ZO2_PERTURB_STREAM, P.base + idx, r);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) classify(j, r[j], j < cnt);
+      }
+      if (PERT) {
+        zx_raw4(P.rs_seed, ZO2_PERTURB_STREAM, P.base + idx, r);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) classify(OFF + j, r[j], j < cnt);
+      }
+    }
+    // queue offsets: warp-inclusive scan of packed (tails | centrals << 16)
+    {
+      const unsigned mine = (unsigned)__popc(tmask) | ((unsigned)__popc(cmask) << 16);
+      unsigned incl = mine;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      unsigned base = 0;
+      if (lane == 31) base = atomicAdd(&sm.counts[buf], incl);
+      base = __shfl_sync(0xffffffffu, base, 31);
+      const unsigned excl = base + incl - mine;
+      unsigned tp = excl & 0xffffu, cp = NSLOT - 1 - (excl >> 16);
+      const int zb0 = zslot(0, t), zb1 = zslot(1, t) - NT;  // even / odd k bases
+#pragma unroll
+      for (int k = 0; k < (UPD ? 4 : 0) + (PERT ? 4 : 0); ++k) {
+        const int zi = ((k & 1) ? zb1 : zb0) + k * NT;
+        if ((tmask >> k) & 1u) sm.q[tp++] = (uint16_t)(zi | (((negmask >> k) & 1u) << 15));
+        if ((cmask >> k) & 1u) sm.q[cp--] = (uint16_t)zi;
+      }
+    }
+    __syncthreads();
+
+    // ---------------- P2: queue (tails, then centrals), 32 entries per warp
+    {
+      const unsigned cnts = sm.counts[buf];
+      const int nt = (int)(cnts & 0xffffu), nc = (int)(cnts >> 16), ntot = nt + nc;
+      int i0 = warp * 32;
+      // chunks holding tail entries (the last one may also hold centrals)
+      for (; i0 < nt; i0 += NT) {
+        const int i = i0 + lane;
+        if (i < nt) {
+          const unsigned e = sm.q[i];
+          const int zi = (int)(e & 0x7FFFu);
+          sm.z[zi] = zx_ndtri_tail(sm.z[zi], (e >> 15) != 0, sm.logtab);
+        } else if (i < ntot) {
+          const int zi = sm.q[NSLOT - nc + (i - nt)];
+          sm.z[zi] = zx_ndtri_central(sm.z[zi], zx_central_coef(ZX_CENTRAL_C));
+        }
+      }
+      if (i0 < ntot) {
+        // pure central chunks: coefficients held in registers across the loop
+        const ZxCentral cc = zx_central_coef(sm.ccoef);
+        for (; i0 < ntot; i0 += NT) {
+          const int i = i0 + lane;
+          if (i < ntot) {
+            const int zi = sm.q[NSLOT - nc + (i - nt)];
+            sm.z[zi] = zx_ndtri_central(sm.z[zi], cc);
+          }
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---------------- P3: apply mapping
+    if (t == 0) sm.counts[buf ^ 1] = 0;  // next tile's queue
+    {
+      const int kind = PERT ? sg.out_kind : ZO2_OUT_NONE;
+      A a[4], ap[4], am[4];
+      int acnt;
+      int wi[4];
+      int zt[4], zj[4];
+      uint64_t o = 0;
+      if (tr) {
+        const int c = t >> 3, rb = 4 * (t & 7);
+        const bool cok = c0 + c < sg.cols;
+        acnt = cok ? (int)min(4u, sg.rows > r0 + rb ? sg.rows - (r0 + rb) : 0u) : 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          wi[i] = (rb + i) * WPITCH + c;
+          zt[i] = (rb + i) * 8 + (c >> 2);
+          zj[i] = c & 3;
+        }
+        o = (uint64_t)(c0 + c) * sg.rows + r0 + rb;
+      } else {
+        acnt = cnt;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          wi[i] = 4 * t + i;
+          zt[i] = t;
+          zj[i] = i;
+        }
+        o = e0 + 4 * (uint64_t)t;
+      }
+      bool slow = false;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[i] = W[wi[i]];
+        ap[i] = am[i] = a[i];
+        if (i < acnt) {
+          const double zu = UPD ? sm.z[zslot(zj[i], zt[i])] : 0.0;
+          const double zp = PERT ? sm.z[zslot(OFF + zj[i], zt[i])] : 0.0;
+          if (a[i] != a[i] || !isfinite(zu) || !isfinite(zp)) {
+            slow = true;
+          } else {
+            chain_fast<UPD, PERT>(a[i], ap[i], am[i], P.ucoef, zu, P.eps, zp);
+          }
+        }
+      }
+      if (slow) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (i >= acnt) continue;
+          const A w0 = W[wi[i]];
+          const double zu = UPD ? sm.z[zslot(zj[i], zt[i])] : 0.0;
+          const double zp = PERT ? sm.z[zslot(OFF + zj[i], zt[i])] : 0.0;
+          if (w0 != w0 || !isfinite(zu) || !isfinite(zp)) {
+            const Chain3<A> c = chain_exact<UPD, PERT, A>(w0, P.ucoef, zu, P.eps, zp);
+            a[i] = c.w;
+            ap[i] = c.wp;
+            am[i] = c.wm;
+          }
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i < acnt) W[wi[i]] = a[i];
+      if (kind != ZO2_OUT_NONE && acnt > 0) emit4<A>(sg, kind, o, ap, am, acnt);
+    }
+    __syncthreads();
+
+    // ---------------- P4: load mapping, restored weights to the arena
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w[j] = W[widx + j];
+    if (vec) Wire<FMT>::store4(arena, idx, w, nn, ns);
+    else
+      for (int j = 0; j < cnt; ++j) Wire<FMT>::store1(arena, idx + j, w[j], nn, ns);
+    // the W buffer read here is rewritten two tiles later, after two barriers
+  }
+}
+
+__device__ __forceinline__ double resolve_ucoef(const double *d_g, double lr, int &upd) {
+  if (!upd) return 0.0;
+  const double g = *d_g;
+  if (upd == 1 && g == 0.0) {
+    upd = 0;
+    return 0.0;
+  }
+  return -(lr * g);
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(NT, ZO2_K2_MINB) k_update_perturb(void *arena, K2Table T, K2Params P,
+                                                          const double *d_g, double lr,
+                                                          uint64_t *counts) {
+  typedef typename Wire<FMT>::A A;
+  __shared__ __align__(16) K2Smem<A> sm;
+  for (int i = threadIdx.x; i < 256; i += NT) sm.logtab[i] = ZO2_LOG_TAB_D[i];
+  if (threadIdx.x < 13) sm.ccoef[threadIdx.x] = ZX_CENTRAL_C[threadIdx.x];
+  if (threadIdx.x < 2) sm.counts[threadIdx.x] = 0;
+  __syncthreads();
+  int upd = P.do_update;
+  P.ucoef = resolve_ucoef(d_g, lr, upd);
+  unsigned nn = 0, ns = 0;
+  if (upd && P.do_perturb) k2_tiles<FMT, true, true>(arena, T, P, sm, nn, ns);
+  else if (upd) k2_tiles<FMT, true, false>(arena, T, P, sm, nn, ns);
+  else if (P.do_perturb) k2_tiles<FMT, false, true>(arena, T, P, sm, nn, ns);
+  else k2_tiles<FMT, false, false>(arena, T, P, sm, nn, ns);
+  if (FMT != ZO2_F32 && FMT != ZO2_F64) add_counts(counts, nn, ns);
+}
+
+template <int FMT>
+int launch_k2(void *arena, const K2Table &T, const K2Params &P, const double *d_g, double lr,
+              uint64_t *counts, cudaStream_t s) {
+  const uint64_t tiles = T.tile_start[T.n];
+  if (tiles == 0) return ZO2_OK;
+  static int occ = 0;
+  if (occ == 0) {
+    ZO2_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_perturb<FMT>, NT, 0));
+    if (occ < 1) occ = 1;
+  }
+  unsigned per_sm = (unsigned)occ;
+  if (g_k2_ctas_per_sm && g_k2_ctas_per_sm < per_sm) per_sm = g_k2_ctas_per_sm;
+  const uint64_t cap = 148ull * per_sm;
+  const unsigned g = (unsigned)(tiles < cap ? tiles : cap);
+  k_update_perturb<FMT><<<g, NT, 0, s>>>(arena, T, P, d_g, lr, counts);
+  zo2_count_launch();
+  ZO2_CHECK_LAUNCH();
+  return ZO2_OK;
+}
+
+}  // namespace
+
+extern "C" int zo2_set_k2_ctas_per_sm(int n) {
+  if (n < 0 || n > 32) return zo2_set_error(ZO2_E_ARG, "zo2_set_k2_ctas_per_sm: 0..32");
+  g_k2_ctas_per_sm = (unsigned)n;
+  return ZO2_OK;
+}
+
+extern "C" int zo2_update_perturb(void *arena, int wire_fmt, uint64_t n, uint64_t base,
+                                  int update, const double *d_g, double lr,
+                                  uint64_t lrs_seed, int perturb, double eps,
+                                  uint64_t rs_seed, const zo2_segment_desc *segs,
+                                  int n_segs, uint64_t *counts, void *cs) {
+  if (n == 0) return ZO2_OK;
+  if (!arena) return zo2_set_error(ZO2_E_ARG, "zo2_update_perturb: null arena");
+  if (update && !d_g) return zo2_set_error(ZO2_E_ARG, "zo2_update_perturb: update needs d_g");
+  if (n_segs < 1 || n_segs > MAX_SEGS)
+    return zo2_set_error(ZO2_E_ARG, "zo2_update_perturb: 1..16 segments required");
+  K2Table T;
+  memset(&T, 0, sizeof(T));
+  uint64_t covered = 0;
+  for (int k = 0; k < n_segs; ++k) {
+    const zo2_segment_desc &sg = segs[k];
+    const uint64_t sn = (uint64_t)sg.rows * sg.cols;
+    if (sg.offset != covered)
+      return zo2_set_error(ZO2_E_ARG, "zo2_update_perturb: segments must tile the bucket in order");
+    covered += sn;
+    const bool t = sg.out_kind == ZO2_OUT_BF16_T || sg.out_kind == ZO2_OUT_SPLIT_T;
+    if (perturb && sg.out_kind != ZO2_OUT_NONE && (!sg.out_plus || !sg.out_minus))
+      return zo2_set_error(ZO2_E_ARG, "zo2_update_perturb: operand outputs missing");
+    if (perturb && (sg.out_kind == ZO2_OUT_SPLIT || sg.out_kind == ZO2_OUT_SPLIT_T) &&
+        (!sg.out_plus_lo || !sg.out_minus_lo))
+      return zo2_set_error(ZO2_E_ARG, "zo2_update_perturb: split lo planes missing");
+    T.s[k] = sg;
+    if (!perturb) T.s[k].out_kind = ZO2_OUT_NONE;
+    T.transposed[k] = (t && perturb) ? 1 : 0;
+    uint64_t tiles;
+    if (T.transposed[k]) {
+      T.tiles_c[k] = (sg.cols + 31) / 32;
+      tiles = (uint64_t)((sg.rows + 31) / 32) * T.tiles_c[k];
+    } else {
+      tiles = (sn + TE - 1) / TE;
+    }
+    T.tile_start[k + 1] = T.tile_start[k] + tiles;
+  }
+  T.n = n_segs;
+  if (covered != n) return zo2_set_error(ZO2_E_ARG, "zo2_update_perturb: segments do not cover n");
+  K2Params P;
+  P.base = base;
+  P.do_update = update;
+  P.ucoef = 0.0;
+  P.lrs_seed = lrs_seed;
+  P.do_perturb = perturb;
+  P.eps = eps;
+  P.rs_seed = rs_seed;
+  cudaStream_t s = (cudaStream_t)cs;
+  switch (wire_fmt) {
+    case ZO2_F64: return launch_k2<ZO2_F64>(arena, T, P, d_g, lr, counts, s);
+    case ZO2_F32: return launch_k2<ZO2_F32>(arena, T, P, d_g, lr, counts, s);
+    case ZO2_BF16: return launch_k2<ZO2_BF16>(arena, T, P, d_g, lr, counts, s);
+    case ZO2_F16: return launch_k2<ZO2_F16>(arena, T, P, d_g, lr, counts, s);
+    case ZO2_F8E4M3: return launch_k2<ZO2_F8E4M3>(arena, T, P, d_g, lr, counts, s);
+    default: return zo2_set_error(ZO2_E_ARG, "zo2_update_perturb: bad wire format");
+  }
+}

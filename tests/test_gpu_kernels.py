@@ -187,6 +187,47 @@ def test_update_only_ungated(cuda, oracle):
         assert np.array_equal(dev.cpu().numpy().view(np.uint32), ref.view(np.uint32))
 
 
+@pytest.mark.parametrize("fmt", ["f32", "bf16"])
+def test_update_perturb_block_scale_matches_axpy_chain(cuda, fmt):
+    """A whole OPT-1.3B-width block (50.4 M parameters, ~100 M draws, ~27 M
+    of them on ndtri's tail branch) through K2 against the same arithmetic
+    as four separate reference-order passes of zo2_axpy_z (per-element
+    Philox + Cephes with IEEE __ddiv_rn/__dsqrt_rn, axpy1 NaN semantics)."""
+    from paper_2503_12668_b200.model import DualForward, ModelSpec, module_size
+    _l = L()
+    spec = ModelSpec(1, 2048, 32, 50272, 512)
+    fwd = DualForward(spec, 1, "f32" if fmt == "f32" else "bf16", cuda, 1)
+    n = module_size(spec, "block.0")
+    base, lrs, rs, eps, lr, g = 103_000_000, 0xABCDEF, 0x13579, 1e-3, 1e-7, 3.75
+    gen = torch.Generator(device=cuda).manual_seed(5)
+    w0 = torch.randn(n, device=cuda, generator=gen) * 0.02
+    w0[:7] = torch.tensor([float("nan"), float("inf"), -float("inf"), 0.0, -0.0, 1e-30, 3e38])
+    arena = w0.clone()
+    d_g = torch.tensor([g], dtype=torch.float64, device=cuda)
+    descs = fwd.block_descs(0)
+    _l.call("zo2_update_perturb", arena.data_ptr(), _l.F32, n, base, 1, d_g.data_ptr(), lr, lrs,
+            1, eps, rs, descs, len(descs), None, stream())
+    ref = w0.clone()
+
+    def axpy(coef, seed):
+        _l.call("zo2_axpy_z", ref.data_ptr(), _l.F32, n, coef, seed, 0, base, stream())
+
+    axpy(-(lr * g), lrs)
+    axpy(eps, rs)
+    wp = ref.clone()
+    axpy(-2.0 * eps, rs)
+    axpy(eps, rs)
+    torch.cuda.synchronize()
+    bad = (arena.view(torch.int32) != ref.view(torch.int32)).nonzero().flatten()
+    assert bad.numel() == 0, f"{bad.numel()} mismatches, first {bad[:5].tolist()}"
+    # the W+ operand of the first weight matrix (qkv_w, [d, 3d] -> [3d, d])
+    from paper_2503_12668_b200.model import block_layout, segments
+    qkv = [sg for sg in segments(block_layout(spec)) if sg.name == "qkv_w"][0]
+    wq = wp[qkv.offset: qkv.offset + qkv.size].view(qkv.shape).t().contiguous()
+    op = fwd.sets[0][1]["qkv_w"][0]
+    assert torch.equal(op.hi.view(-1), wq.view(-1).to(torch.bfloat16))
+
+
 # ------------------------------------------------------------------ K9
 @pytest.mark.parametrize("fmt", ["bf16", "f16", "f8"])
 def test_codecs_bit_exact(cuda, golden, fmt):
