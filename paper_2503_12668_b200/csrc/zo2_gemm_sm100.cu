@@ -27,6 +27,10 @@
 
 void zo2_count_launch(uint64_t n = 1);
 
+#ifndef ZO2_GEMM_SMEM_KB
+#define ZO2_GEMM_SMEM_KB 200  // operand staging budget per CTA
+#endif
+
 namespace {
 
 constexpr int BM = 128;
@@ -138,7 +142,7 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = (SPLIT ? 2 : 1) * (A_BYTES + B_BYTES);
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = (ZO2_GEMM_SMEM_KB * 1024) / STAGE_BYTES > 6 ? 6 : (ZO2_GEMM_SMEM_KB * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -486,7 +490,7 @@ struct Cfg2 {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / 2) * BK * 2;
   static constexpr int STAGE_BYTES = (SPLIT ? 2 : 1) * (A_BYTES + B_BYTES);
-  static constexpr int STAGES = (200 * 1024) / STAGE_BYTES > 6 ? 6 : (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = (ZO2_GEMM_SMEM_KB * 1024) / STAGE_BYTES > 6 ? 6 : (ZO2_GEMM_SMEM_KB * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
 };

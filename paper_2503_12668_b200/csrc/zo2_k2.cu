@@ -72,6 +72,7 @@ struct K2Smem {
   double z[NSLOT];                  // y (reflected uniform) in P1, z after P2
   double logtab[256];               // glibc log (invc, logc) table
   double ccoef[13];                 // central-branch coefficients
+  double tcoef[42];                 // tail-branch coefficients (ZX_TAIL_C)
   A w[2][32 * WPITCH];              // weight tile, double-buffered across tiles
   uint16_t q[NSLOT];                // tail slots from the front, central from the back
   unsigned counts[2];               // packed (n_tail | n_central << 16), per buffer
@@ -320,7 +321,7 @@ __device__ __forceinline__ void k2_tiles(void *arena, const K2Table &T, const K2
         if (i < nt) {
           const unsigned e = sm.q[i];
           const int zi = (int)(e & 0x7FFFu);
-          sm.z[zi] = zx_ndtri_tail(sm.z[zi], (e >> 15) != 0, sm.logtab);
+          sm.z[zi] = zx_ndtri_tail(sm.z[zi], (e >> 15) != 0, sm.logtab, sm.tcoef);
         } else if (i < ntot) {
           const int zi = sm.q[NSLOT - nc + (i - nt)];
           sm.z[zi] = zx_ndtri_central(sm.z[zi], zx_central_coef(ZX_CENTRAL_C));
@@ -435,6 +436,7 @@ __global__ void __launch_bounds__(NT, ZO2_K2_MINB) k_update_perturb(void *arena,
   __shared__ __align__(16) K2Smem<A> sm;
   for (int i = threadIdx.x; i < 256; i += NT) sm.logtab[i] = ZO2_LOG_TAB_D[i];
   if (threadIdx.x < 13) sm.ccoef[threadIdx.x] = ZX_CENTRAL_C[threadIdx.x];
+  if (threadIdx.x < 42) sm.tcoef[threadIdx.x] = ZX_TAIL_C[threadIdx.x];
   if (threadIdx.x < 2) sm.counts[threadIdx.x] = 0;
   __syncthreads();
   int upd = P.do_update;
@@ -454,6 +456,10 @@ int launch_k2(void *arena, const K2Table &T, const K2Params &P, const double *d_
   if (tiles == 0) return ZO2_OK;
   static int occ = 0;
   if (occ == 0) {
+    // maximum shared-memory carveout: an SM configured for this kernel can
+    // also host the persistent GEMM CTA (co-residence on the prepare lane)
+    ZO2_CUDA_TRY(cudaFuncSetAttribute(k_update_perturb<FMT>,
+                                      cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     ZO2_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_perturb<FMT>, NT, 0));
     if (occ < 1) occ = 1;
   }

@@ -237,7 +237,9 @@ class Zo2Engine:
         self.dev = _DeviceStep(workload.spec, workload.arith, runtime.device, self.operand_sets)
         # concurrent prepare lane: one K2 CTA per SM beside the persistent GEMM;
         # otherwise K2 fills the GPU (grid from occupancy)
-        _lib.call("zo2_set_k2_ctas_per_sm", 1 if self.operand_sets >= 2 else 0)
+        import os
+        conc = int(os.environ.get("ZO2_K2_CONCURRENT_CTAS", "1"))
+        _lib.call("zo2_set_k2_ctas_per_sm", conc if self.operand_sets >= 2 else 0)
         self._pool_booked = False
         self._async: list = []
         self._hist = torch.zeros(64, 4, dtype=torch.float64, device=runtime.device)
