@@ -225,7 +225,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                         capacity_bytes=cfg.get("cap", float("inf")), device=dev)
     eng = Zo2Engine(TransformerWorkload(params, cfg["arith"]),
                     ZOConfig(EPS, cfg["lr"], max(1, args.steps), SEED), rt, validate=True,
-                    operand_sets=args.operand_sets)
+                    operand_sets=args.operand_sets, rng=args.rng)
     if world > 1:
         eng.enable_data_parallel()
     ds = gen_synthetic(V, S, 64 * world, RngState(SEED), "affine", B)
@@ -324,7 +324,9 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "parallelism": f"dp{world}" if world > 1 else "single",
                    "wire": cfg["codec"] if cfg["codec"] != "none" else "f32",
                    "compute": "3-pass bf16 split GEMM (f32-faithful)" if split else "bf16 GEMM",
-                   "l2": "inputs larger than L2 (4.8+ GB of weights streamed per step)"},
+                   "l2": "inputs larger than L2 (4.8+ GB of weights streamed per step)",
+                   "rng": args.rng + (" (reference z stream, bit-exact)" if args.rng == "exact"
+                                      else " (Philox4x32 + binary32 erfinv, not the reference's z)")},
         "roofline": {"bound": "tensor", "kernel": "zo2_gemm (tcgen05, fused epilogues)",
                      "achieved": gemm_tflops, "peak": pk["bf16_tflops_sustained"],
                      "unit": "TFLOP/s", "frac": (gemm_tflops / pk["bf16_tflops_sustained"]
@@ -369,6 +371,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--operand-sets", type=int, default=1,
                     help="1: K2 of block i+1 after the forward of block i; 2: concurrent")
+    ap.add_argument("--rng", default="exact", choices=["exact", "fast"],
+                    help="z generator: the reference's stream (default) or the fast GPU one")
     ap.add_argument("--gemm-variant", type=int, default=0,
                     help="0 auto (CTA pair for large shapes), 1 single-CTA, 2 pair")
     args = ap.parse_args()

@@ -68,6 +68,21 @@ int zo2_host_gaussian_fill(double *out, uint64_t n, uint64_t seed,
                            uint64_t stream, uint64_t counter);
 uint64_t zo2_host_derive_step_seed(uint64_t base_seed, uint64_t step_index);
 
+/* z generator used by K2 (update / perturb / restore) and K8 (embedding):
+ *   0 = reference-exact (default): the gaussian_fill stream above;
+ *   1 = fast: Philox4x32-10 + binary32 erfinv (zo2_rng_fast.h) keyed on the
+ *       same (seed, stream, absolute parameter position) -- self-consistent
+ *       across every kernel, statistically equivalent, not the reference's
+ *       values.  No reference counterpart (the reference has one generator).
+ * Process-wide; read at kernel launch. */
+int zo2_set_rng_mode(int mode);
+int zo2_rng_mode(void);
+/* The fast direction itself (binary32), device and host restatement. */
+int zo2_z_fill_fast(float *out, uint64_t n, uint64_t seed, uint64_t stream,
+                    uint64_t counter, void *cuda_stream);
+int zo2_host_z_fill_fast(float *out, uint64_t n, uint64_t seed, uint64_t stream,
+                         uint64_t counter);
+
 /* model.py:198-224 init_params, one segment: out = fmt(std * z) with z drawn
  * at (seed, INIT_STREAM, counter); fmt is ZO2_F32 or ZO2_F64. */
 int zo2_init_normal(void *out, int fmt, uint64_t n, double std, uint64_t seed,
@@ -114,9 +129,9 @@ typedef struct zo2_segment_desc {
  * (naive-mode update pass, finalize drain).  codec conversions tally into
  * d_conv_counts[0] (NaN) and [1] (saturated) if non-null (ConversionSummary,
  * numerics.py:210-217). */
-/* Grid sizing of K2 (148 x n CTAs).  The engine sets 1 when K2 runs on the
- * prepare stream concurrently with the GEMMs, so one K2 CTA and the persistent
- * GEMM CTA co-reside on every SM (FP64/INT pipes vs tensor pipe). */
+/* Grid sizing of K2: 0 (default) = 148 x occupancy CTAs; n = at most n CTAs
+ * per SM (the engine sets 1 when K2 runs on the prepare stream concurrently
+ * with the GEMMs, operand_sets = 2). */
 int zo2_set_k2_ctas_per_sm(int n);
 int zo2_update_perturb(void *arena, int wire_fmt, uint64_t n, uint64_t base,
                        int update, const double *d_g, double lr,

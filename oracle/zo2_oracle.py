@@ -79,6 +79,93 @@ def gauss(seed: int, stream: int, counter: int, n: int) -> np.ndarray:
     return out
 
 
+# ------------------------------------------------------------ rng = "fast"
+# Restatement of paper_2503_12668_b200/csrc/zo2_rng_fast.h (Philox4x32-10 +
+# Giles' single-precision erfinv, every step one IEEE binary32 operation):
+# the B200 fast direction must match it bit for bit.  Not a reference
+# stream -- the reference's z is gauss() above.
+_M32 = 0xFFFFFFFF
+
+
+def fast_raw(seed: int, stream: int, counter: int, n: int) -> np.ndarray:
+    pos = np.uint64(counter & M64) + np.arange(n, dtype=np.uint64)
+    b = pos >> np.uint64(2)
+    c0 = (b & np.uint64(_M32)).astype(np.uint32)
+    c1 = (b >> np.uint64(32)).astype(np.uint32)
+    c2 = np.full(n, stream & _M32, np.uint32)
+    c3 = np.full(n, (stream >> 32) & _M32, np.uint32)
+    k0, k1 = seed & _M32, (seed >> 32) & _M32
+    for _ in range(10):
+        p0 = np.uint64(0xD2511F53) * c0.astype(np.uint64)
+        p1 = np.uint64(0xCD9E8D57) * c2.astype(np.uint64)
+        hi0, lo0 = (p0 >> np.uint64(32)).astype(np.uint32), (p0 & np.uint64(_M32)).astype(np.uint32)
+        hi1, lo1 = (p1 >> np.uint64(32)).astype(np.uint32), (p1 & np.uint64(_M32)).astype(np.uint32)
+        c0, c1, c2, c3 = hi1 ^ c1 ^ np.uint32(k0), lo1, hi0 ^ c3 ^ np.uint32(k1), lo0
+        k0, k1 = (k0 + 0x9E3779B9) & _M32, (k1 + 0xBB67AE85) & _M32
+    lanes = (pos & np.uint64(3)).astype(np.int64)
+    return np.stack([c0, c1, c2, c3], 1)[np.arange(n), lanes]
+
+
+def _f32(x):
+    return np.asarray(x, dtype=np.float32)
+
+
+def _fast_log(a: np.ndarray) -> np.ndarray:
+    ia = a.view(np.uint32)
+    e = ((ia >> np.uint32(23)) & np.uint32(0xFF)).astype(np.int32) - 127
+    im = (ia & np.uint32(0x007FFFFF)) | np.uint32(0x3F800000)
+    big = im > np.uint32(0x3FB504F3)
+    im = np.where(big, im - np.uint32(0x00800000), im).astype(np.uint32)
+    e = e + big.astype(np.int32)
+    m = im.view(np.float32)
+    one = np.float32(1.0)
+    s = (m - one) / (m + one)
+    s2 = s * s
+    p = np.full(a.shape, np.float32(0.11111111), np.float32)
+    for c in (0.14285715, 0.2, 0.33333334, 1.0):
+        p = p * s2 + np.float32(c)
+    lm = (np.float32(2.0) * s) * p
+    return e.astype(np.float32) * np.float32(0.6931472) + lm
+
+
+_GILES_A = (2.81022636e-08, 3.43273939e-07, -3.5233877e-06, -4.39150654e-06, 0.00021858087,
+            -0.00125372503, -0.00417768164, 0.246640727, 1.50140941)
+_GILES_B = (-0.000200214257, 0.000100950558, 0.00134934322, -0.00367342844, 0.00573950773,
+            -0.0076224613, 0.00943887047, 1.00167406, 2.83297682)
+
+
+def fast_gauss_from_raw(r: np.ndarray) -> np.ndarray:
+    r = np.asarray(r, np.uint32)
+    u = ((r >> np.uint32(9)).astype(np.float32) + np.float32(0.5)) * np.float32(1.1920929e-07)
+    x = np.float32(2.0) * u - np.float32(1.0)
+    a = (np.float32(4.0) * u) * (np.float32(1.0) - u)
+    w = np.float32(0.0) - _fast_log(a)
+    lo = w < np.float32(5.0)
+    wa = w - np.float32(2.5)
+    pa = np.full(r.shape, np.float32(_GILES_A[0]), np.float32)
+    for c in _GILES_A[1:]:
+        pa = np.float32(c) + pa * wa
+    wb = np.sqrt(np.where(lo, np.float32(25.0), w)) - np.float32(3.0)
+    pb = np.full(r.shape, np.float32(_GILES_B[0]), np.float32)
+    for c in _GILES_B[1:]:
+        pb = np.float32(c) + pb * wb
+    p = np.where(lo, pa, pb)
+    return np.float32(1.4142135) * (p * x)
+
+
+def fast_gauss(seed: int, stream: int, counter: int, n: int) -> np.ndarray:
+    return fast_gauss_from_raw(fast_raw(seed, stream, counter, n))
+
+
+def axpy_z_fast(flat: np.ndarray, coef: float, seed: int, counter: int) -> None:
+    """flat += coef * z_fast, f64 product and sum, one rounding (model.py:233
+    arithmetic with the fast direction)."""
+    if flat.size == 0:
+        return
+    z = fast_gauss(seed, PERTURB, counter, flat.size).astype(np.float64)
+    flat[:] = (flat.astype(np.float64) + np.float64(coef) * z).astype(flat.dtype)
+
+
 def derive_step_seed(base: int, j: int) -> int:
     return int(lib().oracle_derive_step_seed(base & M64, j & M64))
 
@@ -254,14 +341,15 @@ def batch_for_step(seed, j, n_samples, batch_size):
 class MeZO:
     """zo_ref.py:97-112, sequential restatement."""
 
-    def __init__(self, spec, params, eps, lr, seed):
+    def __init__(self, spec, params, eps, lr, seed, rng="exact"):
         self.spec, self.p, self.eps, self.lr, self.seed = spec, params, eps, lr, seed
         self.losses, self.gs, self.losses_minus = [], [], []
         self.off = offsets(spec)
+        self.axpy = axpy_z_fast if rng == "fast" else axpy_z
 
     def _all(self, coef, s):
         for m, flat in self.p.items():
-            axpy_z(flat, coef, s, self.off[m])
+            self.axpy(flat, coef, s, self.off[m])
 
     def step(self, tokens, targets, j, g_override=None) -> float:
         s = derive_step_seed(self.seed, j)

@@ -57,6 +57,10 @@ _SIGS = {
                                    c_double, c_uint64, c_int, c_double, c_uint64,
                                    POINTER(SegmentDesc), c_int, c_void_p, c_void_p]),
     "zo2_set_k2_ctas_per_sm": (c_int, [c_int]),
+    "zo2_set_rng_mode": (c_int, [c_int]),
+    "zo2_rng_mode": (c_int, []),
+    "zo2_z_fill_fast": (c_int, [c_void_p, c_uint64, c_uint64, c_uint64, c_uint64, c_void_p]),
+    "zo2_host_z_fill_fast": (c_int, [c_void_p, c_uint64, c_uint64, c_uint64, c_uint64]),
     "zo2_encode": (c_int,[c_void_p, c_void_p, c_int, c_uint64, c_void_p, c_void_p]),
     "zo2_decode": (c_int, [c_void_p, c_void_p, c_int, c_uint64, c_void_p]),
     "zo2_form_g": (c_int, [c_void_p, c_double, c_double, c_void_p, c_void_p, c_void_p]),

@@ -8,6 +8,7 @@
 #include "zo2_common.cuh"
 #include "zo2_rng.h"
 #include "zo2_zgen.cuh"
+#include "zo2_rng_fast.h"
 #include <atomic>
 #include <string.h>
 #include <stdio.h>
@@ -88,6 +89,30 @@ extern "C" int zo2_z_fill(double *out, uint64_t n, uint64_t seed, uint64_t strea
   k_z_fill<<<zo2_grid_for(blocks, 256), 256, 0, S(cs)>>>(out, n, seed, stream, counter);
   zo2_count_launch();
   ZO2_CHECK_LAUNCH();
+  return ZO2_OK;
+}
+
+// rng = "fast" direction probe (zo2_rng_fast.h), binary32.
+__global__ void k_z_fill_fast(float *out, uint64_t n, uint64_t seed, uint64_t stream,
+                              uint64_t counter) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = zo2f_gauss_at(seed, stream, counter + i);
+}
+
+extern "C" int zo2_z_fill_fast(float *out, uint64_t n, uint64_t seed, uint64_t stream,
+                               uint64_t counter, void *cs) {
+  if (n == 0) return ZO2_OK;
+  if (!out) return zo2_set_error(ZO2_E_ARG, "zo2_z_fill_fast: null output");
+  k_z_fill_fast<<<zo2_grid_for(n, 256), 256, 0, S(cs)>>>(out, n, seed, stream, counter);
+  zo2_count_launch();
+  ZO2_CHECK_LAUNCH();
+  return ZO2_OK;
+}
+
+extern "C" int zo2_host_z_fill_fast(float *out, uint64_t n, uint64_t seed, uint64_t stream,
+                                    uint64_t counter) {
+  for (uint64_t i = 0; i < n; ++i) out[i] = zo2f_gauss_at(seed, stream, counter + i);
   return ZO2_OK;
 }
 

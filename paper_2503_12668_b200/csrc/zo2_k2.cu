@@ -30,6 +30,7 @@
 #include "zo2_common.cuh"
 #include "zo2_wire.cuh"
 #include "zo2_zexact.cuh"
+#include "zo2_rng_fast.h"
 #include <string.h>
 
 void zo2_count_launch(uint64_t n = 1);
@@ -48,6 +49,9 @@ constexpr int MAX_SEGS = 16;
 // 0 = grid from occupancy; n = at most n CTAs per SM (leave room for a
 // concurrently running persistent GEMM)
 unsigned g_k2_ctas_per_sm = 0;
+// z generator: 0 = reference-exact (Philox4x64-10 + Cephes ndtri), 1 = fast
+// (Philox4x32-10 + binary32 erfinv, zo2_rng_fast.h)
+int g_rng_mode = 0;
 
 struct K2Table {
   zo2_segment_desc s[MAX_SEGS];
@@ -206,7 +210,7 @@ __device__ __forceinline__ void emit4(const zo2_segment_desc &sg, int kind, uint
   }
 }
 
-template <int FMT, bool UPD, bool PERT>
+template <int FMT, bool FAST, bool UPD, bool PERT>
 __device__ __forceinline__ void k2_tiles(void *arena, const K2Table &T, const K2Params &P,
                                          K2Smem<typename Wire<FMT>::A> &sm, unsigned &nn,
                                          unsigned &ns) {
@@ -273,6 +277,29 @@ __device__ __forceinline__ void k2_tiles(void *arena, const K2Table &T, const K2
         if (neg) negmask |= 1u << k;
       }
     };
+    if (FAST) {
+      // rng = "fast": z straight from Philox4x32 + binary32 erfinv, no queue
+      const uint64_t pos = P.base + idx;
+      if (cnt > 0 && (pos & 3) == 0) {
+        uint32_t r[4];
+        if (UPD) {
+          zo2f_philox(P.lrs_seed, ZO2_PERTURB_STREAM, pos >> 2, r);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) sm.z[zslot(j, t)] = (double)zo2f_gauss(r[j]);
+        }
+        if (PERT) {
+          zo2f_philox(P.rs_seed, ZO2_PERTURB_STREAM, pos >> 2, r);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) sm.z[zslot(OFF + j, t)] = (double)zo2f_gauss(r[j]);
+        }
+      } else if (cnt > 0) {  // segment offsets not a multiple of 4 (toy widths)
+        for (int j = 0; j < cnt; ++j) {
+          if (UPD) sm.z[zslot(j, t)] = (double)zo2f_gauss_at(P.lrs_seed, ZO2_PERTURB_STREAM, pos + j);
+          if (PERT) sm.z[zslot(OFF + j, t)] = (double)zo2f_gauss_at(P.rs_seed, ZO2_PERTURB_STREAM, pos + j);
+        }
+      }
+      __syncthreads();
+    } else {
     if (cnt > 0) {
       uint64_t r[4];
       if (UPD) {
@@ -340,70 +367,62 @@ __device__ __forceinline__ void k2_tiles(void *arena, const K2Table &T, const K2
       }
     }
     __syncthreads();
+    }  // !FAST
 
     // ---------------- P3: apply mapping
     if (t == 0) sm.counts[buf ^ 1] = 0;  // next tile's queue
     {
       const int kind = PERT ? sg.out_kind : ZO2_OUT_NONE;
-      A a[4], ap[4], am[4];
-      int acnt;
-      int wi[4];
-      int zt[4], zj[4];
-      uint64_t o = 0;
+      int acnt, wi0, wstep, za[4];
+      uint64_t o;
       if (tr) {
         const int c = t >> 3, rb = 4 * (t & 7);
         const bool cok = c0 + c < sg.cols;
         acnt = cok ? (int)min(4u, sg.rows > r0 + rb ? sg.rows - (r0 + rb) : 0u) : 0;
+        wi0 = rb * WPITCH + c;
+        wstep = WPITCH;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          wi[i] = (rb + i) * WPITCH + c;
-          zt[i] = (rb + i) * 8 + (c >> 2);
-          zj[i] = c & 3;
-        }
+        for (int i = 0; i < 4; ++i) za[i] = zslot(c & 3, (rb + i) * 8 + (c >> 2));
         o = (uint64_t)(c0 + c) * sg.rows + r0 + rb;
       } else {
         acnt = cnt;
+        wi0 = 4 * t;
+        wstep = 1;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          wi[i] = 4 * t + i;
-          zt[i] = t;
-          zj[i] = i;
-        }
+        for (int i = 0; i < 4; ++i) za[i] = zslot(i, t);
         o = e0 + 4 * (uint64_t)t;
       }
-      bool slow = false;
+      // straight-line chain; zslot(OFF + j, t) = zslot(j, t) + OFF * NT (same parity)
+      A a[4], ap[4], am[4];
+      bool bad = false;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        a[i] = W[wi[i]];
-        ap[i] = am[i] = a[i];
-        if (i < acnt) {
-          const double zu = UPD ? sm.z[zslot(zj[i], zt[i])] : 0.0;
-          const double zp = PERT ? sm.z[zslot(OFF + zj[i], zt[i])] : 0.0;
-          if (a[i] != a[i] || !isfinite(zu) || !isfinite(zp)) {
-            slow = true;
-          } else {
-            chain_fast<UPD, PERT>(a[i], ap[i], am[i], P.ucoef, zu, P.eps, zp);
-          }
-        }
+        a[i] = W[wi0 + i * wstep];
+        const double zu = UPD ? sm.z[za[i]] : 0.0;
+        const double zp = PERT ? sm.z[za[i] + OFF * NT] : 0.0;
+        chain_fast<UPD, PERT>(a[i], ap[i], am[i], P.ucoef, zu, P.eps, zp);
+        // a NaN anywhere in the chain (NaN weight, inf - inf) reaches the
+        // restored weight: redo those elements with axpy1's exact NaN rules
+        bad |= (i < acnt) && (a[i] != a[i]);
       }
-      if (slow) {
+      if (bad) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          if (i >= acnt) continue;
-          const A w0 = W[wi[i]];
-          const double zu = UPD ? sm.z[zslot(zj[i], zt[i])] : 0.0;
-          const double zp = PERT ? sm.z[zslot(OFF + zj[i], zt[i])] : 0.0;
-          if (w0 != w0 || !isfinite(zu) || !isfinite(zp)) {
-            const Chain3<A> c = chain_exact<UPD, PERT, A>(w0, P.ucoef, zu, P.eps, zp);
-            a[i] = c.w;
-            ap[i] = c.wp;
-            am[i] = c.wm;
-          }
+          if (i >= acnt || a[i] == a[i]) continue;
+          const double zu = UPD ? sm.z[za[i]] : 0.0;
+          const double zp = PERT ? sm.z[za[i] + OFF * NT] : 0.0;
+          const Chain3<A> c = chain_exact<UPD, PERT, A>(W[wi0 + i * wstep], P.ucoef, zu, P.eps, zp);
+          a[i] = c.w;
+          ap[i] = c.wp;
+          am[i] = c.wm;
         }
       }
+      if (acnt == 4) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i < acnt) W[wi[i]] = a[i];
+        for (int i = 0; i < 4; ++i) W[wi0 + i * wstep] = a[i];
+      } else {
+        for (int i = 0; i < acnt; ++i) W[wi0 + i * wstep] = a[i];
+      }
       if (kind != ZO2_OUT_NONE && acnt > 0) emit4<A>(sg, kind, o, ap, am, acnt);
     }
     __syncthreads();
@@ -428,7 +447,7 @@ __device__ __forceinline__ double resolve_ucoef(const double *d_g, double lr, in
   return -(lr * g);
 }
 
-template <int FMT>
+template <int FMT, bool FAST>
 __global__ void __launch_bounds__(NT, ZO2_K2_MINB) k_update_perturb(void *arena, K2Table T, K2Params P,
                                                           const double *d_g, double lr,
                                                           uint64_t *counts) {
@@ -442,14 +461,14 @@ __global__ void __launch_bounds__(NT, ZO2_K2_MINB) k_update_perturb(void *arena,
   int upd = P.do_update;
   P.ucoef = resolve_ucoef(d_g, lr, upd);
   unsigned nn = 0, ns = 0;
-  if (upd && P.do_perturb) k2_tiles<FMT, true, true>(arena, T, P, sm, nn, ns);
-  else if (upd) k2_tiles<FMT, true, false>(arena, T, P, sm, nn, ns);
-  else if (P.do_perturb) k2_tiles<FMT, false, true>(arena, T, P, sm, nn, ns);
-  else k2_tiles<FMT, false, false>(arena, T, P, sm, nn, ns);
+  if (upd && P.do_perturb) k2_tiles<FMT, FAST, true, true>(arena, T, P, sm, nn, ns);
+  else if (upd) k2_tiles<FMT, FAST, true, false>(arena, T, P, sm, nn, ns);
+  else if (P.do_perturb) k2_tiles<FMT, FAST, false, true>(arena, T, P, sm, nn, ns);
+  else k2_tiles<FMT, FAST, false, false>(arena, T, P, sm, nn, ns);
   if (FMT != ZO2_F32 && FMT != ZO2_F64) add_counts(counts, nn, ns);
 }
 
-template <int FMT>
+template <int FMT, bool FAST>
 int launch_k2(void *arena, const K2Table &T, const K2Params &P, const double *d_g, double lr,
               uint64_t *counts, cudaStream_t s) {
   const uint64_t tiles = T.tile_start[T.n];
@@ -458,16 +477,16 @@ int launch_k2(void *arena, const K2Table &T, const K2Params &P, const double *d_
   if (occ == 0) {
     // maximum shared-memory carveout: an SM configured for this kernel can
     // also host the persistent GEMM CTA (co-residence on the prepare lane)
-    ZO2_CUDA_TRY(cudaFuncSetAttribute(k_update_perturb<FMT>,
+    ZO2_CUDA_TRY(cudaFuncSetAttribute(k_update_perturb<FMT, FAST>,
                                       cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    ZO2_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_perturb<FMT>, NT, 0));
+    ZO2_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_perturb<FMT, FAST>, NT, 0));
     if (occ < 1) occ = 1;
   }
   unsigned per_sm = (unsigned)occ;
   if (g_k2_ctas_per_sm && g_k2_ctas_per_sm < per_sm) per_sm = g_k2_ctas_per_sm;
   const uint64_t cap = 148ull * per_sm;
   const unsigned g = (unsigned)(tiles < cap ? tiles : cap);
-  k_update_perturb<FMT><<<g, NT, 0, s>>>(arena, T, P, d_g, lr, counts);
+  k_update_perturb<FMT, FAST><<<g, NT, 0, s>>>(arena, T, P, d_g, lr, counts);
   zo2_count_launch();
   ZO2_CHECK_LAUNCH();
   return ZO2_OK;
@@ -480,6 +499,13 @@ extern "C" int zo2_set_k2_ctas_per_sm(int n) {
   g_k2_ctas_per_sm = (unsigned)n;
   return ZO2_OK;
 }
+
+extern "C" int zo2_set_rng_mode(int mode) {
+  if (mode != 0 && mode != 1) return zo2_set_error(ZO2_E_ARG, "zo2_set_rng_mode: 0 (exact) or 1 (fast)");
+  g_rng_mode = mode;
+  return ZO2_OK;
+}
+extern "C" int zo2_rng_mode(void) { return g_rng_mode; }
 
 extern "C" int zo2_update_perturb(void *arena, int wire_fmt, uint64_t n, uint64_t base,
                                   int update, const double *d_g, double lr,
@@ -529,12 +555,18 @@ extern "C" int zo2_update_perturb(void *arena, int wire_fmt, uint64_t n, uint64_
   P.eps = eps;
   P.rs_seed = rs_seed;
   cudaStream_t s = (cudaStream_t)cs;
+  const bool fast = g_rng_mode == 1;
   switch (wire_fmt) {
-    case ZO2_F64: return launch_k2<ZO2_F64>(arena, T, P, d_g, lr, counts, s);
-    case ZO2_F32: return launch_k2<ZO2_F32>(arena, T, P, d_g, lr, counts, s);
-    case ZO2_BF16: return launch_k2<ZO2_BF16>(arena, T, P, d_g, lr, counts, s);
-    case ZO2_F16: return launch_k2<ZO2_F16>(arena, T, P, d_g, lr, counts, s);
-    case ZO2_F8E4M3: return launch_k2<ZO2_F8E4M3>(arena, T, P, d_g, lr, counts, s);
+    case ZO2_F64: return fast ? launch_k2<ZO2_F64, true>(arena, T, P, d_g, lr, counts, s)
+                          : launch_k2<ZO2_F64, false>(arena, T, P, d_g, lr, counts, s);
+    case ZO2_F32: return fast ? launch_k2<ZO2_F32, true>(arena, T, P, d_g, lr, counts, s)
+                          : launch_k2<ZO2_F32, false>(arena, T, P, d_g, lr, counts, s);
+    case ZO2_BF16: return fast ? launch_k2<ZO2_BF16, true>(arena, T, P, d_g, lr, counts, s)
+                          : launch_k2<ZO2_BF16, false>(arena, T, P, d_g, lr, counts, s);
+    case ZO2_F16: return fast ? launch_k2<ZO2_F16, true>(arena, T, P, d_g, lr, counts, s)
+                          : launch_k2<ZO2_F16, false>(arena, T, P, d_g, lr, counts, s);
+    case ZO2_F8E4M3: return fast ? launch_k2<ZO2_F8E4M3, true>(arena, T, P, d_g, lr, counts, s)
+                          : launch_k2<ZO2_F8E4M3, false>(arena, T, P, d_g, lr, counts, s);
     default: return zo2_set_error(ZO2_E_ARG, "zo2_update_perturb: bad wire format");
   }
 }

@@ -3,8 +3,10 @@
 // LayerNorm (K4), causal attention (K5), cross-entropy reduction (K7 tail).
 #include "zo2_common.cuh"
 #include "zo2_rng.h"
+#include "zo2_rng_fast.h"
 
 void zo2_count_launch(uint64_t n = 1);
+extern "C" int zo2_rng_mode(void);
 static inline cudaStream_t S(void *s) { return (cudaStream_t)s; }
 
 __device__ __forceinline__ float ax1(float w, double coef, double z) {
@@ -14,27 +16,48 @@ __device__ __forceinline__ float ax1(float w, double coef, double z) {
 // ------------------------------------------------------------------ K8
 // One thread = 4 consecutive columns of one token.  tok and pos elements are
 // regenerated through the module's op sequence: update(lrs) then +eps, -2eps.
+template <bool FAST>
 __device__ __forceinline__ void embed_elem4(const float *table, uint64_t i, uint64_t base,
                                             int upd, double ucoef, uint64_t lrs, double eps,
                                             uint64_t rs, float wp[4], float wm[4]) {
   float4 v = *(const float4 *)(table + i);
   float w[4] = {v.x, v.y, v.z, v.w};
-  uint64_t r[4];
+  double z[4];
   if (upd) {
-    zo2_raw_block(lrs, ZO2_PERTURB_STREAM, (base + i) >> 2, r);
+    if (FAST) {
+      uint32_t r[4];
+      zo2f_philox(lrs, ZO2_PERTURB_STREAM, (base + i) >> 2, r);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) w[j] = ax1(w[j], ucoef, zo2_ndtri(zo2_u53(r[j])));
+      for (int j = 0; j < 4; ++j) z[j] = (double)zo2f_gauss(r[j]);
+    } else {
+      uint64_t r[4];
+      zo2_raw_block(lrs, ZO2_PERTURB_STREAM, (base + i) >> 2, r);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) z[j] = zo2_ndtri(zo2_u53(r[j]));
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w[j] = ax1(w[j], ucoef, z[j]);
   }
-  zo2_raw_block(rs, ZO2_PERTURB_STREAM, (base + i) >> 2, r);
+  if (FAST) {
+    uint32_t r[4];
+    zo2f_philox(rs, ZO2_PERTURB_STREAM, (base + i) >> 2, r);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) z[j] = (double)zo2f_gauss(r[j]);
+  } else {
+    uint64_t r[4];
+    zo2_raw_block(rs, ZO2_PERTURB_STREAM, (base + i) >> 2, r);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) z[j] = zo2_ndtri(zo2_u53(r[j]));
+  }
   const double m2 = -2.0 * eps;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const double z = zo2_ndtri(zo2_u53(r[j]));
-    wp[j] = ax1(w[j], eps, z);
-    wm[j] = ax1(wp[j], m2, z);
+    wp[j] = ax1(w[j], eps, z[j]);
+    wm[j] = ax1(wp[j], m2, z[j]);
   }
 }
 
+template <bool FAST>
 __global__ void k_embed_dual(const int64_t *ids, uint64_t n_tok, uint32_t seq, uint32_t dim,
                              uint32_t vocab, const float *table, uint64_t base, int upd,
                              const double *d_g, double lr, uint64_t lrs, double eps,
@@ -54,8 +77,8 @@ __global__ void k_embed_dual(const int64_t *ids, uint64_t n_tok, uint32_t seq, u
     const int64_t id = ids[t];
     const uint32_t s = (uint32_t)(t % seq);
     float tp[4], tm[4], pp[4], pm[4];
-    embed_elem4(table, (uint64_t)id * dim + c, base, upd, ucoef, lrs, eps, rs, tp, tm);
-    embed_elem4(table, (uint64_t)vocab * dim + (uint64_t)s * dim + c, base, upd, ucoef, lrs,
+    embed_elem4<FAST>(table, (uint64_t)id * dim + c, base, upd, ucoef, lrs, eps, rs, tp, tm);
+    embed_elem4<FAST>(table, (uint64_t)vocab * dim + (uint64_t)s * dim + c, base, upd, ucoef, lrs,
                 eps, rs, pp, pm);
     *(float4 *)(outp + t * dim + c) =
         make_float4(tp[0] + pp[0], tp[1] + pp[1], tp[2] + pp[2], tp[3] + pp[3]);
@@ -75,9 +98,13 @@ extern "C" int zo2_embed_dual(const int64_t *ids, uint64_t n_tok, uint32_t seq, 
   if (seq > max_seq) return zo2_set_error(ZO2_E_ARG, "zo2_embed_dual: seq > max_seq");
   if (update && !d_g) return zo2_set_error(ZO2_E_ARG, "zo2_embed_dual: update needs d_g");
   const uint64_t total = n_tok * (dim / 4);
-  k_embed_dual<<<zo2_grid_for(total, 256, 148u * 16u), 256, 0, S(cs)>>>(
-      ids, n_tok, seq, dim, vocab, table, base, update, d_g, lr, lrs_seed, eps, rs_seed, outp,
-      outm);
+  const unsigned g = zo2_grid_for(total, 256, 148u * 16u);
+  if (zo2_rng_mode() == 1)
+    k_embed_dual<true><<<g, 256, 0, S(cs)>>>(ids, n_tok, seq, dim, vocab, table, base, update,
+                                              d_g, lr, lrs_seed, eps, rs_seed, outp, outm);
+  else
+    k_embed_dual<false><<<g, 256, 0, S(cs)>>>(ids, n_tok, seq, dim, vocab, table, base, update,
+                                               d_g, lr, lrs_seed, eps, rs_seed, outp, outm);
   zo2_count_launch();
   ZO2_CHECK_LAUNCH();
   return ZO2_OK;

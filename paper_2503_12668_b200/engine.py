@@ -33,6 +33,13 @@ from .scheduler import (CudaLanes, Lane, build_iteration_dag, build_prepare_dag,
                         close_step, enqueue_dag, okey, pkey, ukey, validate_timeline)
 
 
+# z generator per engine (zo2b200.h zo2_set_rng_mode): "exact" is the
+# reference's stream (numerics.py:161-182), "fast" the GPU-cost Philox4x32
+# direction; the mode is process-wide in the library and set before every
+# enqueue, so engines with different modes can share a process.
+RNG_MODES = {"exact": 0, "fast": 1}
+
+
 @dataclass(frozen=True)
 class ZOConfig:
     """zo_ref.py:29-42."""
@@ -212,9 +219,12 @@ class Zo2Engine:
     def __init__(self, workload: TransformerWorkload, cfg: ZOConfig, runtime: OffloadRuntime,
                  *, overlap: bool = True, backend: str = "cuda", update_mode: str = "deferred",
                  cost=None, trace=None, validate: bool = True, prepare_lane: bool = True,
-                 operand_sets: int = 2):
+                 operand_sets: int = 2, rng: str = "exact"):
         if update_mode not in ("deferred", "naive"):
             raise ValueError(f"unknown update_mode {update_mode!r}")
+        if rng not in RNG_MODES:
+            raise ValueError(f"unknown rng {rng!r} (one of {tuple(RNG_MODES)})")
+        self.rng = rng
         if overlap and runtime.k_slots < 3:
             raise ValueError("overlap requires at least 3 arena slots")
         if backend != "cuda":
@@ -448,6 +458,7 @@ class Zo2Engine:
 
     def _enqueue(self, batch, step_index: int):
         cfg, rt = self.cfg, self.runtime
+        _lib.call("zo2_set_rng_mode", RNG_MODES[self.rng])
         rt.current_step = step_index
         self.mgr.begin_iteration(derive_step_seed(cfg.seed, step_index))
         comp = self.lanes[Lane.COMPUTE]
@@ -505,6 +516,7 @@ class Zo2Engine:
         """Drain the last pending update (zo2_engine.py:318-336); idempotent."""
         rt = self.runtime
         if self.pending.valid:
+            _lib.call("zo2_set_rng_mode", RNG_MODES[self.rng])
             comp = self.lanes[Lane.COMPUTE]
             for module in self._order:
                 h = self._handles[module]
@@ -555,13 +567,13 @@ class MeZOEngine:
     step equals RefEngine's."""
 
     def __init__(self, workload: TransformerWorkload, cfg: ZOConfig, trace=None, *,
-                 device="cuda", capacity_bytes: float = float("inf")):
+                 device="cuda", capacity_bytes: float = float("inf"), rng: str = "exact"):
         from .runtime import ResidentRuntime
         self.workload, self.cfg, self.trace = workload, cfg, trace
         self.runtime = ResidentRuntime(workload.params, capacity_bytes=capacity_bytes,
                                        device=device)
         k = self.runtime.k_slots
-        self._engine = Zo2Engine(workload, cfg, self.runtime, overlap=k >= 3, trace=trace)
+        self._engine = Zo2Engine(workload, cfg, self.runtime, overlap=k >= 3, trace=trace, rng=rng)
 
     @property
     def losses(self) -> list[float]:

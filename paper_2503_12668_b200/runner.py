@@ -98,13 +98,13 @@ def execute_run(cfg: RunConfig, write_artifacts: bool = True, device="cuda") -> 
     tokens_per_step = cfg.batch_size * cfg.seq_len
     if cfg.engine == "mezo":
         engine = MeZOEngine(workload, zo, device=device,
-                            capacity_bytes=cfg.device_capacity_bytes)
+                            capacity_bytes=cfg.device_capacity_bytes, rng=cfg.rng)
         runtime = engine.runtime
     else:
         runtime = OffloadRuntime(params, k_slots=cfg.arena_slots, codec=cfg.codec,
                                  capacity_bytes=cfg.device_capacity_bytes, device=device)
         engine = Zo2Engine(workload, zo, runtime, overlap=cfg.overlap,
-                           update_mode=cfg.update_mode)
+                           update_mode=cfg.update_mode, rng=cfg.rng)
     t_run0 = time.perf_counter()
     walls = []
     for j in range(cfg.steps):

@@ -8,6 +8,8 @@ sys.path.insert(0, ".")
 from paper_2503_12668_b200 import _lib  # noqa: E402
 from paper_2503_12668_b200.model import DualForward, ModelSpec, module_size  # noqa: E402
 
+import os
+_lib.call("zo2_set_rng_mode", 1 if os.environ.get("ZO2_RNG") == "fast" else 0)
 spec = ModelSpec(1, 2048, 32, 50272, 512)
 fwd = DualForward(spec, 1, "f32", "cuda", 1)
 n = module_size(spec, "block.0")
@@ -28,4 +30,4 @@ for j in range(R):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / R
-print(f"{_lib.LIB_PATH.split('/')[-1]} K2 block ms {ms:.3f}  Gz/s {2 * n / ms / 1e6:.1f}")
+print(f"{_lib.LIB_PATH.split('/')[-1]} rng={os.environ.get('ZO2_RNG', 'exact')} K2 block ms {ms:.3f}  Gz/s {2 * n / ms / 1e6:.1f}")

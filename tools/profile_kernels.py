@@ -32,8 +32,10 @@ def main(arith="f32"):
 
 def k2(arith="f32"):
     """One K2 (update + perturb, transposed operands) over a cfg2 block."""
+    import os
     from paper_2503_12668_b200 import _lib
     from paper_2503_12668_b200.model import module_size
+    _lib.call("zo2_set_rng_mode", 1 if os.environ.get("ZO2_RNG") == "fast" else 0)
     spec = ModelSpec(1, 2048, 32, 50272, 512)
     fwd = DualForward(spec, 16, arith, "cuda", 1)
     n = module_size(spec, "block.0")
