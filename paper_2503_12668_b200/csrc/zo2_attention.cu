@@ -68,8 +68,11 @@ struct AttnCfg {
   static constexpr int SMEM = 2 * STAGE * 2;             // 2 stages, bytes
 };
 
+#ifndef ZO2_ATTN_MINB
+#define ZO2_ATTN_MINB 1
+#endif
 template <int HD, bool SPLIT>
-__global__ void __launch_bounds__(32 * WARPS, 1) k_attn(
+__global__ void __launch_bounds__(32 * WARPS, ZO2_ATTN_MINB) k_attn(
     const __nv_bfloat16 *__restrict__ qkv_hi, const __nv_bfloat16 *__restrict__ qkv_lo,
     uint32_t seq, uint32_t n_heads, __nv_bfloat16 *__restrict__ out_hi,
     __nv_bfloat16 *__restrict__ out_lo) {

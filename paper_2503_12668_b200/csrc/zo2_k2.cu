@@ -90,13 +90,16 @@ __device__ __forceinline__ int zslot(int k, int t) {
   return k * NT + (a << 5) + (b ^ (a | ((k & 1) << 3)));
 }
 
-__device__ __forceinline__ void split_bf16(float x, __nv_bfloat16 &hi, __nv_bfloat16 &lo) {
-  hi = __float2bfloat16_rn(x);
-  lo = __float2bfloat16_rn(x - __bfloat162float(hi));
-}
 
-__device__ __forceinline__ uint32_t pack_bf16(__nv_bfloat16 a, __nv_bfloat16 b) {
-  return (uint32_t)__bfloat16_as_ushort(a) | ((uint32_t)__bfloat16_as_ushort(b) << 16);
+// bf16 pair (a in the low half), one cvt.rn.bf16x2.f32
+__device__ __forceinline__ uint32_t bf16x2(float a, float b) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t *>(&v);
+}
+// hi = bf16(x), lo = bf16(x - f32(hi)) for a pair, as split_bf16
+__device__ __forceinline__ void split_bf16x2(float a, float b, uint32_t &hi, uint32_t &lo) {
+  hi = bf16x2(a, b);
+  lo = bf16x2(a - __uint_as_float(hi << 16), b - __uint_as_float(hi & 0xFFFF0000u));
 }
 
 // Element chain without the per-op NaN checks (finite weights and z); the
@@ -172,39 +175,38 @@ __device__ __forceinline__ void emit4(const zo2_segment_desc &sg, int kind, uint
       }
     }
   } else if (kind == ZO2_OUT_BF16 || kind == ZO2_OUT_BF16_T) {
-    __nv_bfloat16 p[4], m[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      p[j] = __float2bfloat16_rn((float)wp[j]);
-      m[j] = __float2bfloat16_rn((float)wm[j]);
-    }
+    // one cvt.rn.bf16x2.f32 per pair (same bits as two __float2bfloat16_rn)
+    const uint32_t p01 = bf16x2((float)wp[0], (float)wp[1]), p23 = bf16x2((float)wp[2], (float)wp[3]);
+    const uint32_t m01 = bf16x2((float)wm[0], (float)wm[1]), m23 = bf16x2((float)wm[2], (float)wm[3]);
     if (cnt == 4 && (o & 3) == 0) {
-      *(uint2 *)((__nv_bfloat16 *)sg.out_plus + o) = make_uint2(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]));
-      *(uint2 *)((__nv_bfloat16 *)sg.out_minus + o) = make_uint2(pack_bf16(m[0], m[1]), pack_bf16(m[2], m[3]));
+      *(uint2 *)((__nv_bfloat16 *)sg.out_plus + o) = make_uint2(p01, p23);
+      *(uint2 *)((__nv_bfloat16 *)sg.out_minus + o) = make_uint2(m01, m23);
     } else {
+      const uint32_t pv[2] = {p01, p23}, mv[2] = {m01, m23};
       for (int j = 0; j < cnt; ++j) {
-        ((__nv_bfloat16 *)sg.out_plus)[o + j] = p[j];
-        ((__nv_bfloat16 *)sg.out_minus)[o + j] = m[j];
+        ((uint16_t *)sg.out_plus)[o + j] = (uint16_t)(pv[j >> 1] >> (16 * (j & 1)));
+        ((uint16_t *)sg.out_minus)[o + j] = (uint16_t)(mv[j >> 1] >> (16 * (j & 1)));
       }
     }
   } else if (kind == ZO2_OUT_SPLIT || kind == ZO2_OUT_SPLIT_T) {
-    __nv_bfloat16 ph[4], pl[4], mh[4], ml[4];
+    uint32_t ph[2], pl[2], mh[2], ml[2];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      split_bf16((float)wp[j], ph[j], pl[j]);
-      split_bf16((float)wm[j], mh[j], ml[j]);
+    for (int j = 0; j < 2; ++j) {
+      split_bf16x2((float)wp[2 * j], (float)wp[2 * j + 1], ph[j], pl[j]);
+      split_bf16x2((float)wm[2 * j], (float)wm[2 * j + 1], mh[j], ml[j]);
     }
     if (cnt == 4 && (o & 3) == 0) {
-      *(uint2 *)((__nv_bfloat16 *)sg.out_plus + o) = make_uint2(pack_bf16(ph[0], ph[1]), pack_bf16(ph[2], ph[3]));
-      *(uint2 *)((__nv_bfloat16 *)sg.out_plus_lo + o) = make_uint2(pack_bf16(pl[0], pl[1]), pack_bf16(pl[2], pl[3]));
-      *(uint2 *)((__nv_bfloat16 *)sg.out_minus + o) = make_uint2(pack_bf16(mh[0], mh[1]), pack_bf16(mh[2], mh[3]));
-      *(uint2 *)((__nv_bfloat16 *)sg.out_minus_lo + o) = make_uint2(pack_bf16(ml[0], ml[1]), pack_bf16(ml[2], ml[3]));
+      *(uint2 *)((__nv_bfloat16 *)sg.out_plus + o) = make_uint2(ph[0], ph[1]);
+      *(uint2 *)((__nv_bfloat16 *)sg.out_plus_lo + o) = make_uint2(pl[0], pl[1]);
+      *(uint2 *)((__nv_bfloat16 *)sg.out_minus + o) = make_uint2(mh[0], mh[1]);
+      *(uint2 *)((__nv_bfloat16 *)sg.out_minus_lo + o) = make_uint2(ml[0], ml[1]);
     } else {
       for (int j = 0; j < cnt; ++j) {
-        ((__nv_bfloat16 *)sg.out_plus)[o + j] = ph[j];
-        ((__nv_bfloat16 *)sg.out_plus_lo)[o + j] = pl[j];
-        ((__nv_bfloat16 *)sg.out_minus)[o + j] = mh[j];
-        ((__nv_bfloat16 *)sg.out_minus_lo)[o + j] = ml[j];
+        const int w = j >> 1, sh = 16 * (j & 1);
+        ((uint16_t *)sg.out_plus)[o + j] = (uint16_t)(ph[w] >> sh);
+        ((uint16_t *)sg.out_plus_lo)[o + j] = (uint16_t)(pl[w] >> sh);
+        ((uint16_t *)sg.out_minus)[o + j] = (uint16_t)(mh[w] >> sh);
+        ((uint16_t *)sg.out_minus_lo)[o + j] = (uint16_t)(ml[w] >> sh);
       }
     }
   }
