@@ -223,6 +223,10 @@ int zo2_ce_reduce(const float *ce_part, uint32_t M, uint32_t n_tiles,
 /* model.py:273-283 causal softmax attention on packed qkv given as bf16
  * planes [B*S, 3d] (hi, and lo when split; heads split as reshape(B,S,H,hd)),
  * writing ctx as an A operand (bf16 hi, + lo when split). */
+/* 0 (default): the tcgen05/TMEM attention kernel where it applies (seq a
+ * multiple of 128, head_dim 64, or 128 without split planes), else the
+ * mma.sync kernel; 1: mma.sync kernel only (A/B). */
+int zo2_set_attention_variant(int variant);
 int zo2_attention(const void *qkv_hi, const void *qkv_lo, uint32_t batch,
                   uint32_t seq, uint32_t n_heads, uint32_t head_dim,
                   void *ctx_hi, void *ctx_lo, void *cuda_stream);

@@ -13,6 +13,15 @@
 #include "zo2_common.cuh"
 
 void zo2_count_launch(uint64_t n = 1);
+extern "C" int zo2_attention_tc(const void *qkv_hi, const void *qkv_lo, uint32_t batch,
+                                uint32_t seq, uint32_t n_heads, uint32_t head_dim, void *ctx_hi,
+                                void *ctx_lo, void *cs);
+static int g_attn_variant = 0;  // 0: tcgen05 kernel where eligible, 1: mma.sync kernel only
+extern "C" int zo2_set_attention_variant(int v) {
+  if (v < 0 || v > 1) return zo2_set_error(ZO2_E_ARG, "zo2_set_attention_variant: 0 or 1");
+  g_attn_variant = v;
+  return ZO2_OK;
+}
 
 namespace {
 
@@ -350,6 +359,17 @@ extern "C" int zo2_attention(const void *qkv_hi, const void *qkv_lo, uint32_t ba
     return zo2_set_error(ZO2_E_ARG, "zo2_attention: lo planes must be given for in and out");
   cudaStream_t s = (cudaStream_t)cs;
   int rc = ZO2_OK;
+  if (g_attn_variant == 0) {
+    // tcgen05 / TMEM kernel (zo2_gemm_sm100.cu) for seq % 128 == 0, hd 64 / 128
+    rc = zo2_attention_tc(qkv_hi, qkv_lo, batch, seq, n_heads, head_dim, ctx_hi, ctx_lo, cs);
+    if (rc == ZO2_OK) {
+      zo2_count_launch();
+      ZO2_CHECK_LAUNCH();
+      return ZO2_OK;
+    }
+    if (rc != ZO2_E_UNSUPPORTED) return rc;
+    rc = ZO2_OK;
+  }
   switch (head_dim) {
     case 16: rc = split ? launch<16, true>(qkv_hi, qkv_lo, batch, seq, n_heads, ctx_hi, ctx_lo, s)
                         : launch<16, false>(qkv_hi, qkv_lo, batch, seq, n_heads, ctx_hi, ctx_lo, s); break;

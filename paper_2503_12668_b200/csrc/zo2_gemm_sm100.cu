@@ -803,7 +803,352 @@ int dispatch_epi2(const GemmArgs &a, int epi, cudaStream_t s) {
 
 int g_variant = 0;  // 0 auto, 1 single-CTA only, 2 CTA pair whenever legal
 
+
+// ====================================================================== K5 (tcgen05)
+// Causal attention of one (q-tile of 128 queries, head, batch) on the 5th-gen
+// tensor cores (model.py:273-283):  S = Q K^T -> softmax(S / sqrt(hd)) -> P V.
+//   * Q, K, V tiles come straight from the QKV GEMM's bf16 planes ([T, 3d]:
+//     q | k | v column blocks) by TMA (128-byte swizzle, 64-column panels);
+//     V is consumed MN-major (hd contiguous), so it is never transposed.
+//   * S (128 x 128 f32) and O (128 x hd f32) live in TMEM; 4 warps own 32
+//     TMEM lanes (= query rows) each and run the softmax from tcgen05.ld.
+//   * two passes over the causal key tiles: the first takes the row max of
+//     the full S, the second recomputes S, writes P = exp(S - max) to shared
+//     memory (bf16, swizzled K-major A operand) and accumulates O += P V, so O
+//     is never rescaled.  Split (f32-faithful) mode: S = Qh Kh + Qh Kl + Ql Kh,
+//     O += Ph Vh + Ph Vl + Pl Vh (~2^-16 relative per product, as the GEMMs).
+//   * one thread issues TMA and MMAs; completion is tracked with mbarriers.
+struct AttnTcArgs {
+  CUtensorMap tq[2];  // qkv hi / lo planes, [T, 3d], box 64 x 128 (query tile)
+  CUtensorMap tk[2];  // same planes, box 64 x 64 (key / value tile)
+  __nv_bfloat16 *out_hi, *out_lo;
+  uint32_t seq, n_heads, dim;
+  float scale_log2;   // log2(e) / sqrt(hd)
+};
+
+constexpr int ATT_Q = 128;  // queries per CTA (TMEM lanes)
+constexpr int ATT_K = 64;   // keys per tile
+constexpr int ATT_T = ATT_Q;
+
+// Instruction descriptor: bf16 x bf16 -> f32, M = 128, N = n; b_mn: B MN-major.
+__host__ __device__ constexpr uint32_t idesc_bf16_b(int n, bool b_mn) {
+  return idesc_bf16(n) | (b_mn ? (1u << 16) : 0u);
+}
+// MN-major 128B-swizzle descriptor: 8-row K groups 1024 B apart (SBO), 64-element
+// MN groups `lbo` bytes apart (LBO).
+__device__ __forceinline__ uint64_t sw128_desc_mn(uint32_t saddr, uint32_t lbo) {
+  return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int HD, bool SPLIT>
+struct AttnTcCfg {
+  static constexpr int PL = SPLIT ? 2 : 1;               // planes
+  static constexpr int PAN = HD / 64;                    // 64-column panels of hd
+  static constexpr int QTILE = ATT_Q * 128;              // one 128-row panel, bytes
+  static constexpr int KTILE = ATT_K * 128;              // one 64-row panel
+  static constexpr int KV = PL * PAN * KTILE;            // K (or V) tile, all planes
+  static constexpr int PB = PL * QTILE;                  // P [128 q x 64 keys], all planes
+  static constexpr int NS = 3;                           // K/V ring stages
+  static constexpr int Q_OFF = 0;
+  static constexpr int KV_OFF = Q_OFF + PL * PAN * QTILE;  // stage s: K at +2s*KV, V at +(2s+1)*KV
+  static constexpr int P_OFF = KV_OFF + NS * 2 * KV;       // 2 P buffers
+  static constexpr int BAR_OFF = P_OFF + 2 * PB;
+  static constexpr int SMEM = BAR_OFF + 256 + 4 * 128 * 4 + 1024;
+  static constexpr uint32_t TMEM_COLS = 256;             // S 2 x 64 + O hd (<= 128)
+};
+
+// 8 softmax warps (warp w and w + 4 share TMEM lane quadrant w % 4 = 32 query
+// rows and split the 64 columns of S and the hd columns of O) + 1 warp that
+// issues TMA and tcgen05.mma; the two sides meet only on mbarriers.
+constexpr int ATT_SOFT = 256;
+template <int HD, bool SPLIT>
+__global__ void __launch_bounds__(ATT_SOFT + 32, 1) k_attn_tc(const __grid_constant__ AttnTcArgs a) {
+  using C = AttnTcCfg<HD, SPLIT>;
+  constexpr int NS = C::NS;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t *bar_kv = (uint64_t *)(smem + C::BAR_OFF);  // [NS] tile loaded (TMA)
+  uint64_t *bar_s = bar_kv + NS;                       // [2]  S written (MMA commit)
+  uint64_t *bar_sfree = bar_s + 2;                     // [2]  S read (256 arrivals)
+  uint64_t *bar_p = bar_sfree + 2;                     // [2]  P written (256 arrivals)
+  uint64_t *bar_o = bar_p + 2;                         // [2]  P.V done (MMA commit)
+  uint32_t *tmem_slot = (uint32_t *)(bar_o + 2);
+  float *xch = (float *)(smem + C::BAR_OFF + 256);     // [2][128] row max, then [2][128] row sum
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // heavy (late) query tiles first
+  const uint32_t qt = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+  const int row0 = (int)(b * a.seq + qt * ATT_Q);
+  const uint32_t n_kt = (qt + 1) * (ATT_Q / ATT_K);  // causal: key tiles up to the diagonal
+  const uint32_t n_all = 2 * n_kt;                   // pass 1 (K only) then pass 2 (K, V)
+  const uint32_t d = a.dim;
+
+  if (threadIdx.x == ATT_SOFT) {
+    for (int i = 0; i < NS; ++i) mbar_init(&bar_kv[i], 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar_s[i], 1);
+      mbar_init(&bar_sfree[i], ATT_SOFT);
+      mbar_init(&bar_p[i], ATT_SOFT);
+      mbar_init(&bar_o[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int p = 0; p < C::PL; ++p) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tq[p]) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tk[p]) : "memory");
+    }
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)), "r"(C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_o = tmem + 128;
+
+  if (warp == ATT_SOFT / 32) {
+    // ================================================ TMA + MMA issue (one thread)
+    if (lane == 0) {
+      const uint32_t sq = smem_u32(smem + C::Q_OFF), skv = smem_u32(smem + C::KV_OFF),
+                     sp = smem_u32(smem + C::P_OFF);
+      auto load_tile = [&](uint32_t g) {
+        const uint32_t j = g < n_kt ? g : g - n_kt;
+        const bool with_v = g >= n_kt, with_q = g == 0;
+        const int st = (int)(g % NS);
+        const uint32_t bytes = (uint32_t)C::KV * (with_v ? 2u : 1u) +
+                               (with_q ? (uint32_t)(C::PL * C::PAN * C::QTILE) : 0u);
+        mbar_expect_tx(&bar_kv[st], bytes);
+        const int krow = (int)(b * a.seq + j * ATT_K);
+        uint8_t *kb = smem + C::KV_OFF + 2 * st * C::KV;
+        for (int p = 0; p < C::PL; ++p)
+          for (int c = 0; c < C::PAN; ++c) {
+            const int o = (p * C::PAN + c) * C::KTILE;
+            if (with_q)
+              tma_load_2d(smem + C::Q_OFF + (p * C::PAN + c) * C::QTILE, &a.tq[p], &bar_kv[st],
+                          (int)(h * HD + 64 * c), row0);
+            tma_load_2d(kb + o, &a.tk[p], &bar_kv[st], (int)(d + h * HD + 64 * c), krow);
+            if (with_v)
+              tma_load_2d(kb + C::KV + o, &a.tk[p], &bar_kv[st],
+                          (int)(2 * d + h * HD + 64 * c), krow);
+          }
+      };
+      // S[g & 1] = Q K(g)^T (3 passes split); K-major A and B
+      auto issue_qk = [&](uint32_t g) {
+        constexpr uint32_t id = idesc_bf16_b(ATT_K, false);
+        const uint32_t ts = tmem + (g & 1u) * ATT_K;
+        const uint32_t sk = skv + (uint32_t)(2 * (int)(g % NS) * C::KV);
+        for (int ks = 0; ks < HD / 16; ++ks) {
+          const uint32_t qo = (uint32_t)((ks / 4) * C::QTILE + (ks % 4) * 32);
+          const uint32_t ko = (uint32_t)((ks / 4) * C::KTILE + (ks % 4) * 32);
+          const uint64_t qa = sw128_desc(sq + qo), kd = sw128_desc(sk + ko);
+          tc_mma(ts, qa, kd, id, ks != 0);
+          if (SPLIT) {
+            tc_mma(ts, qa, sw128_desc(sk + C::PAN * C::KTILE + ko), id, 1u);
+            tc_mma(ts, sw128_desc(sq + C::PAN * C::QTILE + qo), kd, id, 1u);
+          }
+        }
+        tc_commit(&bar_s[g & 1u]);
+      };
+      // O += P(j) V(j): A = P [128 q x 64 keys] K-major, B = V [64 keys x hd] MN-major
+      auto issue_pv = [&](uint32_t g) {
+        const uint32_t j = g - n_kt, pb = j & 1u;
+        constexpr uint32_t id = idesc_bf16_b(HD, true);
+        constexpr uint32_t vlbo = (uint32_t)C::KTILE;  // next 64 hd columns: next panel
+        const uint32_t sv = skv + (uint32_t)((2 * (int)(g % NS) + 1) * C::KV);
+        const uint32_t spb = sp + pb * (uint32_t)C::PB;
+        for (int ks = 0; ks < ATT_K / 16; ++ks) {
+          const uint32_t poff = (uint32_t)(ks * 32);
+          const uint32_t voff = (uint32_t)(ks * 16 * 128);  // 16 keys x 128 B
+          const uint64_t pa = sw128_desc(spb + poff), vb = sw128_desc_mn(sv + voff, vlbo);
+          tc_mma(t_o, pa, vb, id, (j | (uint32_t)ks) != 0);
+          if (SPLIT) {
+            tc_mma(t_o, pa, sw128_desc_mn(sv + C::PAN * C::KTILE + voff, vlbo), id, 1u);
+            tc_mma(t_o, sw128_desc(spb + C::QTILE + poff), vb, id, 1u);
+          }
+        }
+        tc_commit(&bar_o[pb]);
+      };
+
+      for (uint32_t g = 0; g < (uint32_t)NS && g < n_all; ++g) load_tile(g);
+      for (uint32_t g = 0; g < n_all; ++g) {
+        // S(g): K(g) loaded, S buffer g & 1 drained (tile g - 2 read by softmax)
+        mbar_wait(&bar_kv[g % NS], (g / NS) & 1u);
+        if (g >= 2) mbar_wait(&bar_sfree[g & 1u], ((g - 2) >> 1) & 1u);
+        tc_fence_after();
+        issue_qk(g);
+        if (g >= n_kt) {
+          // P.V of this tile once the softmax wrote P(j)
+          const uint32_t j = g - n_kt;
+          mbar_wait(&bar_p[j & 1u], (j >> 1) & 1u);
+          tc_fence_after();
+          issue_pv(g);
+          if (g + NS < n_all) {
+            mbar_wait(&bar_o[j & 1u], (j >> 1) & 1u);  // stage g % NS read by P.V
+            load_tile(g + NS);
+          }
+        } else if (g + NS < n_all) {
+          mbar_wait(&bar_s[g & 1u], (g >> 1) & 1u);  // stage g % NS read by S(g)
+          load_tile(g + NS);
+        }
+      }
+    }
+  } else {
+    // ================================================ softmax warps
+    const int quad = warp & 3, half = warp >> 2;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const int r = quad * 32 + lane;  // query row within the tile (TMEM lane)
+    const int c0 = 32 * half;        // this warp's 32 columns of S
+    float mrow = -INFINITY, mscaled = 0.f, lsum = 0.f;
+    for (uint32_t g = 0; g < n_all; ++g) {
+      const bool pass2 = g >= n_kt;
+      const uint32_t j = pass2 ? g - n_kt : g;
+      const int lim = (int)(qt * ATT_Q) + r - (int)(j * ATT_K) - c0;  // visible: i <= lim
+      mbar_wait(&bar_s[g & 1u], (g >> 1) & 1u);
+      tc_fence_after();
+      uint32_t v[32];
+      tmem_ld32(tmem + (g & 1u) * ATT_K + lane_base + (uint32_t)c0, v);
+      tc_fence_before();
+      mbar_arrive(&bar_sfree[g & 1u]);
+      if (!pass2) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i <= lim) mrow = fmaxf(mrow, __uint_as_float(v[i]));
+        if (g + 1 == n_kt) {
+          xch[half * 128 + r] = mrow;
+          asm volatile("bar.sync 1, %0;" ::"n"(ATT_SOFT) : "memory");
+          mscaled = fmaxf(xch[r], xch[128 + r]) * a.scale_log2;
+        }
+        continue;
+      }
+      // P(j) -> smem buffer j & 1 once P.V(j - 2) released it
+      const uint32_t pb = j & 1u;
+      if (j >= 2) mbar_wait(&bar_o[pb], ((j - 2) >> 1) & 1u);
+      uint8_t *prow = smem + C::P_OFF + pb * C::PB + (r >> 3) * 1024 + (r & 7) * 128;
+      float pv[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float e = (i <= lim) ? ex2f(__uint_as_float(v[i]) * a.scale_log2 - mscaled) : 0.f;
+        pv[i] = e;
+        lsum += e;
+      }
+      const int kc = c0 >> 3;  // first 16-byte chunk of these 32 keys
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float x0 = pv[8 * q + 2 * e], x1 = pv[8 * q + 2 * e + 1];
+          const __nv_bfloat162 hv = __floats2bfloat162_rn(x0, x1);
+          hi[e] = *reinterpret_cast<const uint32_t *>(&hv);
+          if (SPLIT) {
+            const __nv_bfloat162 lv = __floats2bfloat162_rn(x0 - __low2float(hv),
+                                                            x1 - __high2float(hv));
+            lo[e] = *reinterpret_cast<const uint32_t *>(&lv);
+          }
+        }
+        const int chunk = (kc + q) ^ (r & 7);
+        *(uint4 *)(prow + chunk * 16) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        if (SPLIT)
+          *(uint4 *)(prow + C::QTILE + chunk * 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&bar_p[pb]);
+    }
+    // ---------------------------------------------- epilogue: O / l -> bf16 planes
+    xch[256 + half * 128 + r] = lsum;
+    {
+      const uint32_t jl = n_kt - 1;
+      mbar_wait(&bar_o[jl & 1u], (jl >> 1) & 1u);  // last P.V (and so every P.V) done
+      tc_fence_after();
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(ATT_SOFT) : "memory");
+    const float inv = 1.0f / (xch[256 + r] + xch[384 + r]);
+    __nv_bfloat16 *oh = a.out_hi + (uint64_t)(row0 + r) * d + h * HD;
+    __nv_bfloat16 *ol = SPLIT ? a.out_lo + (uint64_t)(row0 + r) * d + h * HD : nullptr;
+#pragma unroll 1
+    for (int o0 = half * (HD / 2); o0 < (half + 1) * (HD / 2); o0 += 32) {
+      uint32_t w[32];
+      tmem_ld32(t_o + lane_base + (uint32_t)o0, w);
+      uint32_t hi[16], lo[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const float x0 = __uint_as_float(w[2 * e]) * inv, x1 = __uint_as_float(w[2 * e + 1]) * inv;
+        const __nv_bfloat162 hv = __floats2bfloat162_rn(x0, x1);
+        hi[e] = *reinterpret_cast<const uint32_t *>(&hv);
+        const __nv_bfloat162 lv = __floats2bfloat162_rn(x0 - __low2float(hv), x1 - __high2float(hv));
+        lo[e] = *reinterpret_cast<const uint32_t *>(&lv);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        *(uint4 *)(oh + o0 + 8 * q) = make_uint4(hi[4 * q], hi[4 * q + 1], hi[4 * q + 2], hi[4 * q + 3]);
+        if (SPLIT)
+          *(uint4 *)(ol + o0 + 8 * q) = make_uint4(lo[4 * q], lo[4 * q + 1], lo[4 * q + 2], lo[4 * q + 3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(C::TMEM_COLS)
+                 : "memory");
+}
+
+template <int HD, bool SPLIT>
+int launch_attn_tc(const void *qh, const void *ql, uint32_t batch, uint32_t seq, uint32_t nh,
+                   void *oh, void *ol, cudaStream_t s) {
+  using C = AttnTcCfg<HD, SPLIT>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_attn_tc<HD, SPLIT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return zo2_set_cuda_error(e);
+    attr = true;
+  }
+  AttnTcArgs a;
+  memset(&a, 0, sizeof(a));
+  const uint32_t d = nh * HD, T = batch * seq;
+  int rc = make_map(qh, T, 3 * d, (uint32_t)ATT_Q, &a.tq[0]);
+  if (!rc) rc = make_map(qh, T, 3 * d, (uint32_t)ATT_K, &a.tk[0]);
+  if (!rc && SPLIT) rc = make_map(ql, T, 3 * d, (uint32_t)ATT_Q, &a.tq[1]);
+  if (!rc && SPLIT) rc = make_map(ql, T, 3 * d, (uint32_t)ATT_K, &a.tk[1]);
+  if (rc) return rc;
+  a.out_hi = (__nv_bfloat16 *)oh;
+  a.out_lo = (__nv_bfloat16 *)ol;
+  a.seq = seq;
+  a.n_heads = nh;
+  a.dim = d;
+  a.scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
+  dim3 grid(seq / ATT_Q, nh, batch);
+  k_attn_tc<HD, SPLIT><<<grid, ATT_SOFT + 32, C::SMEM, s>>>(a);
+  return ZO2_OK;
+}
 }  // namespace
+
+
+// tcgen05 attention (K5) for seq % 128 == 0 and head_dim 64 (split or bf16) or
+// 128 (bf16); returns ZO2_E_UNSUPPORTED otherwise (the caller falls back).
+extern "C" int zo2_attention_tc(const void *qkv_hi, const void *qkv_lo, uint32_t batch,
+                                uint32_t seq, uint32_t n_heads, uint32_t head_dim, void *ctx_hi,
+                                void *ctx_lo, void *cs) {
+  const bool split = qkv_lo != nullptr;
+  if (seq % ATT_T != 0 || seq == 0) return ZO2_E_UNSUPPORTED;
+  cudaStream_t s = (cudaStream_t)cs;
+  if (head_dim == 64)
+    return split ? launch_attn_tc<64, true>(qkv_hi, qkv_lo, batch, seq, n_heads, ctx_hi, ctx_lo, s)
+                 : launch_attn_tc<64, false>(qkv_hi, qkv_lo, batch, seq, n_heads, ctx_hi, ctx_lo, s);
+  if (head_dim == 128 && !split)
+    return launch_attn_tc<128, false>(qkv_hi, qkv_lo, batch, seq, n_heads, ctx_hi, ctx_lo, s);
+  return ZO2_E_UNSUPPORTED;
+}
 
 extern "C" int zo2_gemm_tile_n(int split) {
   (void)split;

@@ -395,7 +395,7 @@ def test_layernorm(cuda, dim):
 
 
 @pytest.mark.parametrize("split", [True, False])
-@pytest.mark.parametrize("B,S,H,hd", [(2, 16, 4, 8), (2, 128, 12, 64), (1, 512, 4, 128),
+@pytest.mark.parametrize("B,S,H,hd", [(2, 16, 4, 8), (2, 128, 12, 64), (1, 512, 4, 128), (2, 512, 4, 64),
                                       (2, 200, 3, 64), (1, 64, 2, 32), (3, 96, 2, 16)])
 def test_attention(cuda, B, S, H, hd, split):
     d = H * hd

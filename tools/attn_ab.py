@@ -7,6 +7,8 @@ import torch
 sys.path.insert(0, ".")
 from paper_2503_12668_b200 import _lib  # noqa: E402
 
+import os
+_lib.call("zo2_set_attention_variant", int(os.environ.get("ZO2_ATTN_VARIANT", "0")))
 for B, S, H, hd, split in ((16, 512, 32, 64, True), (16, 512, 32, 128, False)):
     d = H * hd
     T = B * S
@@ -27,5 +29,5 @@ for B, S, H, hd, split in ((16, 512, 32, 64, True), (16, 512, 32, 128, False)):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 20
     fl = 2 * 2 * B * H * S * S * hd / 2  # causal useful FLOPs (QK^T + PV)
-    print(f"{_lib.LIB_PATH.split('/')[-2]} hd={hd} split={split}: {ms * 1e3:.1f} us  "
+    print(f"variant={os.environ.get('ZO2_ATTN_VARIANT', '0')} hd={hd} split={split}: {ms * 1e3:.1f} us  "
           f"{fl / ms / 1e9:.0f} TFLOP/s causal-useful")
