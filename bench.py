@@ -45,6 +45,14 @@ CONFIGS = {
     "cfg4": dict(workload="OPT-30B ZO2 offload, bf16 compute/wire, 18 GB HBM cap, 16 x 512",
                  spec=(48, 7168, 56, 50272, 512), B=16, arith="bf16", codec="bf16", lr=1e-7,
                  slots=3, cap=18e9),
+    # OPT-175B: the full 96 blocks need 348 GB of pinned fp16 masters; the GPU
+    # boxes of this pool have 196 GB of host RAM, so the bench runs 24 of the 96
+    # full-width blocks and also reports the full-depth step extrapolated from
+    # the measured per-block time (blocks are identical work units)
+    "cfg5": dict(workload="OPT-175B geometry ZO2 offload, fp16 host masters, bf16 compute, "
+                          "16 x 512, 24 of 96 blocks (host RAM)",
+                 spec=(24, 12288, 96, 50272, 512), B=16, arith="bf16", codec="f16", lr=1e-7,
+                 slots=3, full_blocks=96),
 }
 EPS, SEED = 1e-3, 1
 
@@ -155,6 +163,28 @@ def cpu_step_sample(spec_t, B, lr):
             f"at batch {bsub} (x{scale:g}), resident-module RNG scaled by size; "
             f"estimate = {nb} x block + embed + head")
     return total, desc
+
+
+def full_depth_estimate(tls, cfg, tokens_step):
+    """Step time of the full-depth model from the measured timelines: the
+    per-block period (compute-lane start of block i+1 minus that of block i,
+    median over the timed steps) x the missing blocks, added to the measured
+    step (embedding, head and the measured blocks included)."""
+    from paper_2503_12668_b200.scheduler import Lane
+    periods, steps = [], []
+    for tl in tls:
+        cs = sorted((e.t_start, e.module) for e in tl.events
+                    if e.lane is Lane.COMPUTE and e.module.startswith("block."))
+        periods += [b[0] - a[0] for a, b in zip(cs, cs[1:])]
+        steps.append(tl.makespan if hasattr(tl, "makespan") else
+                     max(e.t_end for e in tl.events) - min(e.t_start for e in tl.events))
+    if not periods:
+        return None
+    per_block = statistics.median(periods)
+    nb, full = cfg["spec"][0], cfg["full_blocks"]
+    step = statistics.median(steps) + (full - nb) * per_block
+    return {"blocks_measured": nb, "blocks_full": full, "per_block_ms": per_block * 1e3,
+            "step_ms": step * 1e3, "tokens_per_s": tokens_step / step}
 
 
 def cpu_threads():
@@ -368,6 +398,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                 "note": "h2d/d2h include the per-step block weight traffic of the offload"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
+        **({"full_depth_extrapolation": full_depth_estimate(tls, cfg, T * world)}
+           if cfg.get("full_blocks") else {}),
         "losses_tail": eng.losses[-2:],
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
