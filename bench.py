@@ -249,15 +249,39 @@ def run_ours(args, cfg, rank, world, local_rank):
     B = cfg["B"]
     T = B * S
     # with a codec the blocks are encoded on device straight into pinned low-bit
-    # masters (no f32 host copy: OPT-30B f32 masters alone exceed host RAM)
-    params = init_params(spec, RngState(SEED), device=dev, codec=cfg["codec"])
+    # masters (no f32 host copy: OPT-30B f32 masters alone exceed host RAM).
+    # Data parallel: one node-wide shared copy of the masters (local rank 0
+    # creates and fills it), each rank moving only its slice over PCIe.
+    shm = None
+    if world > 1 and not args.replicated_masters:
+        from paper_2503_12668_b200.model import block_id, module_size
+        from paper_2503_12668_b200.runtime import _TORCH_STORAGE, SharedHostMasters
+        from paper_2503_12668_b200.numerics import CODEC_FORMATS, ElemFormat
+        name = [f"zo2_masters_{os.getpid()}_{int(time.time())}" if rank == 0 else None]
+        dist.broadcast_object_list(name, src=0)
+        sdt = _TORCH_STORAGE[CODEC_FORMATS[cfg["codec"]] if cfg["codec"] != "none"
+                             else ElemFormat.F32]
+        n_elem = module_size(spec, block_id(0))
+        if rank == 0:
+            shm = SharedHostMasters(name[0], nb, n_elem, sdt, owner=True)
+            params = init_params(spec, RngState(SEED), device=dev, codec=cfg["codec"],
+                                 host_masters=shm)
+            dist.barrier()
+        else:
+            dist.barrier()
+            shm = SharedHostMasters(name[0], nb, n_elem, sdt, owner=False)
+            params = init_params(spec, RngState(SEED), device=dev, codec=cfg["codec"],
+                                 host_masters=shm)
+    else:
+        params = init_params(spec, RngState(SEED), device=dev, codec=cfg["codec"])
     rt = OffloadRuntime(params, k_slots=cfg["slots"], codec=cfg["codec"],
                         capacity_bytes=cfg.get("cap", float("inf")), device=dev)
     eng = Zo2Engine(TransformerWorkload(params, cfg["arith"]),
                     ZOConfig(EPS, cfg["lr"], max(1, args.steps), SEED), rt, validate=True,
                     operand_sets=args.operand_sets, rng=args.rng)
+    sharded = False
     if world > 1:
-        eng.enable_data_parallel()
+        sharded = eng.enable_data_parallel(shard_transfers=shm is not None)
     ds = gen_synthetic(V, S, 64 * world, RngState(SEED), "affine", B)
     from paper_2503_12668_b200.parallel import shard_indices
 
@@ -316,8 +340,10 @@ def run_ours(args, cfg, rank, world, local_rank):
     # per-step timeline metrics: H2D GB/s from upload events, GPU idle %
     up = [e for tl in tls for e in tl.events if e.lane is Lane.UPLOAD]
     off = [e for tl in tls for e in tl.events if e.lane is Lane.OFFLOAD]
-    h2d_gbs = (sum(rt.block_nbytes for _ in up) / sum(e.duration for e in up) / 1e9) if up else None
-    d2h_gbs = (sum(rt.block_nbytes for _ in off) / sum(e.duration for e in off) / 1e9) if off else None
+    # host-link bytes this rank moved per block transfer (1/world of the block
+    # with sharded transfers; the upload event also covers the NVLink all-gather)
+    h2d_gbs = (sum(rt.wire_nbytes for _ in up) / sum(e.duration for e in up) / 1e9) if up else None
+    d2h_gbs = (sum(rt.wire_nbytes for _ in off) / sum(e.duration for e in off) / 1e9) if off else None
     comp_busy = sum(tl.lane_busy(Lane.COMPUTE) for tl in tls)
     idle_pct = max(0.0, 100.0 * (1.0 - comp_busy / (dev_ms * 1e-3))) if tls else None
 
@@ -335,7 +361,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     tokens_step = T * world
     value = tokens_step * args.steps / (ms * 1e-3)
     e2e_value = tokens_step * args.steps / e2e_s
-    wire_per_dir = nb * rt.block_nbytes
+    wire_per_dir = nb * rt.wire_nbytes
     # step roofline: slower of offloaded bytes at the measured
     # host link and algorithmic GEMM FLOPs at the bf16 tensor peak
     flops_step = 2 * (nb * (24.0 * T * d * d + 4.0 * B * S * S * d) + 2.0 * T * d * V)
@@ -364,7 +390,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         "dtype": "f32" if split else "bf16", "data": "synthetic",
         "config": {"workload": cfg["workload"], "model": f"OPT geometry {nb}x{d}, V={V}",
                    "global_batch": B * world, "seq_len": S,
-                   "parallelism": f"dp{world}" if world > 1 else "single",
+                   "parallelism": (f"dp{world}" + (" (shared masters, sharded PCIe + NVLink "
+                                                   "all-gather)" if sharded else "")
+                                   if world > 1 else "single"),
                    "wire": cfg["codec"] if cfg["codec"] != "none" else "f32",
                    "compute": "3-pass bf16 split GEMM (f32-faithful)" if split else "bf16 GEMM",
                    "l2": "inputs larger than L2 (4.8+ GB of weights streamed per step)",
@@ -413,6 +441,10 @@ def run_ours(args, cfg, rank, world, local_rank):
                                 "kind": "port", "sample": desc}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if shm is not None:
+        torch.cuda.synchronize()
+        dist.barrier()
+        shm.close()
 
 
 def main():
@@ -425,6 +457,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--operand-sets", type=int, default=1,
                     help="1: K2 of block i+1 after the forward of block i; 2: concurrent")
+    ap.add_argument("--replicated-masters", action="store_true",
+                    help="data parallel: private host masters per rank and full-block "
+                         "transfers (default: one shared copy, sharded transfers)")
     ap.add_argument("--rng", default="exact", choices=["exact", "fast"],
                     help="z generator: the reference's stream (default) or the fast GPU one")
     ap.add_argument("--gemm-variant", type=int, default=0,

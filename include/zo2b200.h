@@ -139,6 +139,13 @@ int zo2_update_perturb(void *arena, int wire_fmt, uint64_t n, uint64_t base,
                        uint64_t rs_seed, const zo2_segment_desc *segs,
                        int n_segs, uint64_t *d_conv_counts, void *cuda_stream);
 
+/* ======================= host tier ===================================== */
+/* cudaHostRegister(ptr, bytes, portable) / cudaHostUnregister: pins the
+ * node-wide shared block masters of a data-parallel job (runtime.py
+ * HostBlockStore, one copy per node instead of one per rank). */
+int zo2_host_register(void *ptr, uint64_t bytes);
+int zo2_host_unregister(void *ptr);
+
 /* ======================= K9: wire codecs ================================= */
 /* numerics.py:281-311 encode/decode; fmt in {ZO2_F16, ZO2_BF16, ZO2_F8E4M3}. */
 int zo2_encode(const float *src, void *dst, int fmt, uint64_t n,

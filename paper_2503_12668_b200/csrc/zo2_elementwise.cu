@@ -297,6 +297,20 @@ extern "C" int zo2_axpy_z(void *w, int fmt, uint64_t n, double coef, uint64_t se
   return ZO2_OK;
 }
 
+// ------------------------------------------------------------------ host pinning
+// Page-locks an existing host range (the node-wide shared block masters of a
+// data-parallel job, runtime.SharedHostMasters) so cudaMemcpyAsync moves it by
+// DMA at full PCIe rate; portable = usable from every device of the process.
+extern "C" int zo2_host_register(void *ptr, uint64_t bytes) {
+  if (!ptr || bytes == 0) return zo2_set_error(ZO2_E_ARG, "zo2_host_register: empty range");
+  ZO2_CUDA_TRY(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable));
+  return ZO2_OK;
+}
+extern "C" int zo2_host_unregister(void *ptr) {
+  ZO2_CUDA_TRY(cudaHostUnregister(ptr));
+  return ZO2_OK;
+}
+
 // ------------------------------------------------------------------ K10
 __global__ void k_form_g(const double *sums, double count, double eps, double *out,
                          int *flag) {

@@ -257,13 +257,21 @@ class Zo2Engine:
         self.dist_group = None
         self.world = 1
 
-    def enable_data_parallel(self, group=None) -> None:
+    def enable_data_parallel(self, group=None, shard_transfers: bool = False) -> bool:
         """Shard the batch over torch.distributed ranks: every rank perturbs with
         the same seed and applies the same g; only the two f64 loss sums cross
-        NVLink (one NCCL all-reduce per step on the compute stream)."""
+        NVLink (one NCCL all-reduce per step on the compute stream).
+
+        shard_transfers (node-wide shared masters, runtime.SharedHostMasters):
+        each rank also moves only its 1/world slice of every block over PCIe and
+        completes the arena with an NVLink all-gather.  Returns whether the
+        transfers are sharded."""
         import torch.distributed as dist
         self.dist_group = group or dist.group.WORLD
         self.world = dist.get_world_size(self.dist_group)
+        if shard_transfers and not getattr(self.runtime, "resident", False):
+            return self.runtime.enable_sharding(dist.get_rank(self.dist_group), self.world)
+        return False
 
     # -- bookkeeping of one module visit (zo2_engine.py:187-203) -------------
     def _visit(self, module: str, step: int) -> tuple[RngState, RngState | None, bool]:

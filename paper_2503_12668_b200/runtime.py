@@ -153,15 +153,57 @@ class ModelParams:
         return cls(spec, dev(flats[EMBED_ID]), blocks, dev(head))
 
 
+class SharedHostMasters:
+    """One node-wide copy of the block masters for data-parallel ranks.
+
+    Every rank holds bit-identical weights (same z, same all-reduced g), so a
+    per-rank private master (N x the host RAM, N x the host-DRAM traffic) is
+    redundant: the masters live in one POSIX shared-memory file that every
+    local rank maps and page-locks (zo2_host_register).  With sharded
+    transfers (OffloadRuntime.enable_sharding) rank r uploads and offloads only
+    slice r of each block, and the arenas are completed over NVLink; rank r's
+    slice of the master is written only by rank r, so no cross-process
+    ordering on host memory is needed.  Local rank 0 creates and initialises
+    the file (`owner`); SURVEY.md 8(e)."""
+
+    def __init__(self, name: str, n_blocks: int, block_elems: int, dtype: torch.dtype,
+                 owner: bool):
+        import os
+        self.path = f"/dev/shm/{name}"
+        self.owner = owner
+        esize = torch.empty((), dtype=dtype).element_size()
+        total = n_blocks * block_elems
+        if owner:
+            with open(self.path, "wb") as f:
+                f.truncate(total * esize)
+        self.flat = torch.from_file(self.path, shared=True, size=total, dtype=dtype)
+        self.nbytes = total * esize
+        _lib.call("zo2_host_register", self.flat.data_ptr(), self.nbytes)
+        self.blocks = [self.flat[i * block_elems:(i + 1) * block_elems] for i in range(n_blocks)]
+        self._os = os
+
+    def close(self) -> None:
+        if self.flat is not None:
+            _lib.call("zo2_host_unregister", self.flat.data_ptr())
+            self.flat = None
+            self.blocks = []
+            if self.owner and self._os.path.exists(self.path):
+                self._os.unlink(self.path)
+
+
 def init_params(spec: ModelSpec, state: RngState, fmt: ElemFormat = ElemFormat.F32,
-                device="cuda", pin: bool = True, codec: str | None = None) -> ModelParams:
+                device="cuda", pin: bool = True, codec: str | None = None,
+                host_masters: "SharedHostMasters | None" = None) -> ModelParams:
     """model.py:198-224 on device: bit-identical buckets, blocks then moved to
     pinned host memory (the offload tier).
 
     With `codec`, each block is encoded on the device straight into its pinned
     low-bit host master (exactly HostBlockStore's encode at construction,
     runtime.py:154-162) so the f32 block copy never exists on the host --
-    required for OPT-30B/175B, whose f32 masters would not fit in host RAM."""
+    required for OPT-30B/175B, whose f32 masters would not fit in host RAM.
+
+    With `host_masters` (data parallel, one copy per node) the blocks are the
+    shared file's views; only its owner writes them."""
     if fmt is not ElemFormat.F32:
         raise ValueError("the B200 engine keeps parameters in f32 (arith f32 / bf16)")
     seed = state.seed
@@ -178,15 +220,22 @@ def init_params(spec: ModelSpec, state: RngState, fmt: ElemFormat = ElemFormat.F
     enc = torch.empty(n, dtype=_TORCH_STORAGE[cfmt], device=device) if cfmt else None
     s = torch.cuda.current_stream().cuda_stream
     for i in range(spec.n_blocks):
+        if host_masters is not None:
+            host = host_masters.blocks[i]
+            if not host_masters.owner:
+                blocks.append(host)
+                continue
         init_module_(spec, block_id(i), seed, scratch)
         if cfmt is None:
-            host = torch.empty(n, dtype=torch.float32, pin_memory=pin)
+            if host_masters is None:
+                host = torch.empty(n, dtype=torch.float32, pin_memory=pin)
             host.copy_(scratch)
         else:
             _lib.call("zo2_encode", scratch.data_ptr(), enc.data_ptr(), cfmt.code, n,
                       conv.data_ptr(), s)
-            host = torch.empty(n, dtype=enc.dtype, pin_memory=pin)
-            host.copy_(enc)
+            if host_masters is None:
+                host = torch.empty(n, dtype=enc.dtype, pin_memory=pin)
+            host.copy_(enc.view(host.dtype))
         blocks.append(host)
     torch.cuda.synchronize()
     p = ModelParams(spec, emb, blocks, head, fmt)
@@ -213,6 +262,8 @@ def params_digest(params) -> str:
 class OffloadRuntime:
     """Pinned host masters + K device arenas + transfer log + pool, for one run
     (runtime.py:202-304 surface)."""
+
+    shard = None  # (rank, world, group, lo, hi) once enable_sharding() succeeded
 
     def __init__(self, params: ModelParams, *, k_slots: int = 3, codec: str | None = None,
                  capacity_bytes: float = float("inf"), device="cuda"):
@@ -264,9 +315,46 @@ class OffloadRuntime:
         self._slot_owner: list[str | None] = [None] * self.k_slots
         self._pending_records: list[tuple[TransferRecord, str]] = []
 
+    def enable_sharding(self, rank: int, world: int, group=None) -> bool:
+        """Data parallel with node-wide shared masters: rank r moves only slice r
+        of every block over PCIe (H2D and D2H) and the arena is completed with
+        one NVLink all-gather on the upload lane.  Per-rank
+        host-link bytes drop by `world`; every rank's arena still holds the
+        whole block, bit-identical across ranks.  Needs block_size % world ==
+        0 (d % 8 == 0 and world | 8); returns False (replicated transfers)
+        otherwise."""
+        import torch.distributed as dist
+        if world <= 1 or self.block_size % world != 0:
+            return False
+        n = self.block_size // world
+        # a communicator of its own: the arena all-gathers queue behind each
+        # other, never behind the compute lane's loss all-reduce
+        g = dist.new_group(list(range(world))) if group is None else group
+        self.shard = (rank, world, g, rank * n, (rank + 1) * n)
+        return True
+
+    def _gather(self, slot: int) -> None:
+        import torch.distributed as dist
+        rank, world, g, lo, hi = self.shard
+        full = self.slots[slot].view(torch.uint8)
+        esize = self.slots[slot].element_size()
+        mine = full[lo * esize:hi * esize]
+        if dist.get_backend(g) == "nccl":
+            dist.all_gather_into_tensor(full, mine, group=g)  # in place
+        else:  # gloo (CPU tests / ranks sharing one GPU)
+            parts = list(full.chunk(world))
+            dist.all_gather(parts, mine.clone(), group=g)
+
     @property
     def block_nbytes(self) -> int:
         return self.block_size * self.wire_fmt.bytes_per_elem
+
+    @property
+    def wire_nbytes(self) -> int:
+        """Host-link bytes of one block transfer on this rank."""
+        if self.shard is None:
+            return self.block_nbytes
+        return self.block_nbytes // self.shard[1]
 
     def slot_for(self, block_index: int) -> int:
         return block_index % self.k_slots
@@ -285,9 +373,14 @@ class OffloadRuntime:
                 f"upload of {module} into slot {slot} still owned by "
                 f"{self._slot_owner[slot]} (scheduler bug)")
         with torch.cuda.stream(stream):
-            self.slots[slot].copy_(self.host[module], non_blocking=True)
+            if self.shard is None:
+                self.slots[slot].copy_(self.host[module], non_blocking=True)
+            else:
+                lo, hi = self.shard[3], self.shard[4]
+                self.slots[slot][lo:hi].copy_(self.host[module][lo:hi], non_blocking=True)
+                self._gather(slot)
         self._slot_owner[slot] = module
-        rec = TransferRecord(module, "upload", self.block_nbytes, self.wire_fmt, 0.0, 0.0, step)
+        rec = TransferRecord(module, "upload", self.wire_nbytes, self.wire_fmt, 0.0, 0.0, step)
         self._pending_records.append((rec, key or f"U:{module}"))
 
     def offload(self, module: str, slot: int, step: int, stream: torch.cuda.Stream,
@@ -297,9 +390,13 @@ class OffloadRuntime:
                 f"offload of {module} from slot {slot} owned by {self._slot_owner[slot]} "
                 f"(scheduler bug)")
         with torch.cuda.stream(stream):
-            self.host[module].copy_(self.slots[slot], non_blocking=True)
+            if self.shard is None:
+                self.host[module].copy_(self.slots[slot], non_blocking=True)
+            else:
+                lo, hi = self.shard[3], self.shard[4]
+                self.host[module][lo:hi].copy_(self.slots[slot][lo:hi], non_blocking=True)
         self._slot_owner[slot] = None
-        rec = TransferRecord(module, "offload", self.block_nbytes, self.wire_fmt, 0.0, 0.0, step)
+        rec = TransferRecord(module, "offload", self.wire_nbytes, self.wire_fmt, 0.0, 0.0, step)
         self._pending_records.append((rec, key or f"O:{module}"))
 
     def take_records(self) -> list:
