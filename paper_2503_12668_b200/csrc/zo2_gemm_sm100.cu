@@ -978,25 +978,37 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 1) k_attn_tc(const __grid_const
       };
 
       for (uint32_t g = 0; g < (uint32_t)NS && g < n_all; ++g) load_tile(g);
+      mbar_wait(&bar_kv[0], 0);
+      tc_fence_after();
+      issue_qk(0);
       for (uint32_t g = 0; g < n_all; ++g) {
-        // S(g): K(g) loaded, S buffer g & 1 drained (tile g - 2 read by softmax)
-        mbar_wait(&bar_kv[g % NS], (g / NS) & 1u);
-        if (g >= 2) mbar_wait(&bar_sfree[g & 1u], ((g - 2) >> 1) & 1u);
-        tc_fence_after();
-        issue_qk(g);
-        if (g >= n_kt) {
-          // P.V of this tile once the softmax wrote P(j)
+        // refill the ring stage of tile g - 1 (consumed by S(g - 1) / P.V(g - 1)).
+        // Done before S(g + 1) is issued: S(g + 1) shares bar_s with S(g - 1),
+        // and a parity wait must never trail its barrier by two phases.
+        if (g >= 1 && g - 1 + NS < n_all) {
+          const uint32_t gp = g - 1;
+          if (gp >= n_kt) {
+            const uint32_t jp = gp - n_kt;
+            mbar_wait(&bar_o[jp & 1u], (jp >> 1) & 1u);
+          } else {
+            mbar_wait(&bar_s[gp & 1u], (gp >> 1) & 1u);
+          }
+          load_tile(gp + NS);
+        }
+        // S(g + 1) next, so it runs while the softmax warps work on S(g):
+        // needs K(g + 1) and the S buffer of tile g - 1 drained
+        if (g + 1 < n_all) {
+          const uint32_t gn = g + 1;
+          mbar_wait(&bar_kv[gn % NS], (gn / NS) & 1u);
+          if (gn >= 2) mbar_wait(&bar_sfree[gn & 1u], ((gn - 2) >> 1) & 1u);
+          tc_fence_after();
+          issue_qk(gn);
+        }
+        if (g >= n_kt) {  // P.V of this tile once the softmax wrote P(j)
           const uint32_t j = g - n_kt;
           mbar_wait(&bar_p[j & 1u], (j >> 1) & 1u);
           tc_fence_after();
           issue_pv(g);
-          if (g + NS < n_all) {
-            mbar_wait(&bar_o[j & 1u], (j >> 1) & 1u);  // stage g % NS read by P.V
-            load_tile(g + NS);
-          }
-        } else if (g + NS < n_all) {
-          mbar_wait(&bar_s[g & 1u], (g >> 1) & 1u);  // stage g % NS read by S(g)
-          load_tile(g + NS);
         }
       }
     }
