@@ -253,15 +253,26 @@ def run_ours(args, cfg, rank, world, local_rank):
     # Data parallel: one node-wide shared copy of the masters (local rank 0
     # creates and fills it), each rank moving only its slice over PCIe.
     shm = None
-    if world > 1 and not args.replicated_masters:
+    use_shm = world > 1 and not args.replicated_masters
+    if use_shm:
         from paper_2503_12668_b200.model import block_id, module_size
         from paper_2503_12668_b200.runtime import _TORCH_STORAGE, SharedHostMasters
         from paper_2503_12668_b200.numerics import CODEC_FORMATS, ElemFormat
-        name = [f"zo2_masters_{os.getpid()}_{int(time.time())}" if rank == 0 else None]
-        dist.broadcast_object_list(name, src=0)
         sdt = _TORCH_STORAGE[CODEC_FORMATS[cfg["codec"]] if cfg["codec"] != "none"
                              else ElemFormat.F32]
         n_elem = module_size(spec, block_id(0))
+        need = nb * n_elem * torch.empty((), dtype=sdt).element_size()
+        name = [None, True]
+        if rank == 0:
+            st = os.statvfs("/dev/shm") if os.path.isdir("/dev/shm") else None
+            name = [f"zo2_masters_{os.getpid()}_{int(time.time())}",
+                    st is not None and st.f_bavail * st.f_frsize > need * 1.05]
+            if not name[1]:
+                print(f"bench: /dev/shm cannot hold {need / 1e9:.1f} GB of shared masters; "
+                      f"using per-rank masters", file=sys.stderr)
+        dist.broadcast_object_list(name, src=0)
+        use_shm = bool(name[1])
+    if use_shm:
         if rank == 0:
             shm = SharedHostMasters(name[0], nb, n_elem, sdt, owner=True)
             params = init_params(spec, RngState(SEED), device=dev, codec=cfg["codec"],

@@ -21,6 +21,14 @@ def _free_port():
 
 
 def _worker(rank, world, port, sharded, codec, q):
+    try:
+        q.put((rank, _body(rank, world, port, sharded, codec)))
+    except Exception as e:  # surface the failure instead of a queue timeout
+        import traceback
+        q.put((rank, {"error": f"{e!r}\n{traceback.format_exc()}"}))
+
+
+def _body(rank, world, port, sharded, codec):
     import torch.distributed as dist
     from paper_2503_12668_b200.data import gen_synthetic
     from paper_2503_12668_b200.engine import TransformerWorkload, ZOConfig, Zo2Engine
@@ -64,7 +72,7 @@ def _worker(rank, world, port, sharded, codec, q):
     if shm is not None:
         shm.close()
     dist.destroy_process_group()
-    q.put((rank, out))
+    return out
 
 
 def _run(sharded, codec=None):
@@ -74,9 +82,15 @@ def _run(sharded, codec=None):
     ps = [ctx.Process(target=_worker, args=(r, 2, port, sharded, codec, q)) for r in range(2)]
     for p in ps:
         p.start()
-    res = dict(q.get(timeout=300) for _ in ps)
-    for p in ps:
-        p.join(timeout=60)
+    try:
+        res = dict(q.get(timeout=300) for _ in ps)
+    finally:
+        for p in ps:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    for r, out in res.items():
+        assert "error" not in out, f"rank {r}: {out['error']}"
     return res
 
 
