@@ -42,8 +42,11 @@ constexpr int TE = 1024;         // elements per tile (32 x 32, or 1024 linear)
 constexpr int NSLOT = 8 * NT;    // draw slots per tile (update 4 + perturb 4 per thread)
 constexpr int WPITCH = 33;       // W tile row pitch (conflict-free transposed reads)
 constexpr int MAX_SEGS = 16;
+#ifndef ZO2_K2_CENTRAL_X2
+#define ZO2_K2_CENTRAL_X2 1
+#endif
 #ifndef ZO2_K2_MINB
-#define ZO2_K2_MINB 3  // 80 registers: no spills; 3 CTAs (24 warps) per SM
+#define ZO2_K2_MINB 4  // 64 registers (a few spills in cold paths): 4 CTAs (32 warps) per SM
 #endif
 
 // 0 = grid from occupancy; n = at most n CTAs per SM (leave room for a
@@ -359,6 +362,19 @@ __device__ __forceinline__ void k2_tiles(void *arena, const K2Table &T, const K2
       if (i0 < ntot) {
         // pure central chunks: coefficients held in registers across the loop
         const ZxCentral cc = zx_central_coef(sm.ccoef);
+#if ZO2_K2_CENTRAL_X2
+        // two entries per lane per trip: two independent FP64 chains in flight
+        for (; i0 + NT < ntot; i0 += 2 * NT) {
+          const int ia = i0 + lane, ib = i0 + NT + lane;
+          const int za = sm.q[NSLOT - nc + (ia - nt)];
+          const bool vb = ib < ntot;
+          const int zb = vb ? sm.q[NSLOT - nc + (ib - nt)] : za;
+          const double ra = zx_ndtri_central(sm.z[za], cc);
+          const double rb = zx_ndtri_central(sm.z[zb], cc);
+          sm.z[za] = ra;
+          if (vb) sm.z[zb] = rb;
+        }
+#endif
         for (; i0 < ntot; i0 += NT) {
           const int i = i0 + lane;
           if (i < ntot) {
