@@ -165,6 +165,36 @@ def cpu_step_sample(spec_t, B, lr):
     return total, desc
 
 
+def link_probe(dev, nbytes=1 << 30, reps=3):
+    """Pinned host <-> device copy rate of this box, both directions at once
+    (full duplex, as in the step): best of `reps` 1 GiB copies, CUDA events on
+    each copy stream.  The link term of the step roofline uses this capability,
+    not the rate the step's own transfers happened to reach."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    dbuf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    dbuf2 = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    su, so = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    best_up = best_dn = 0.0
+    for _ in range(reps):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        torch.cuda.synchronize(dev)
+        with torch.cuda.stream(su):
+            ev[0].record(su)
+            dbuf.copy_(h, non_blocking=True)
+            ev[1].record(su)
+        with torch.cuda.stream(so):
+            ev[2].record(so)
+            h2.copy_(dbuf2, non_blocking=True)
+            ev[3].record(so)
+        torch.cuda.synchronize(dev)
+        best_up = max(best_up, nbytes / (ev[0].elapsed_time(ev[1]) * 1e-3) / 1e9)
+        best_dn = max(best_dn, nbytes / (ev[2].elapsed_time(ev[3]) * 1e-3) / 1e9)
+    del h, h2, dbuf, dbuf2
+    return best_up, best_dn
+
+
 def full_depth_estimate(tls, cfg, tokens_step):
     """Step time of the full-depth model from the measured timelines: the
     per-block period (compute-lane start of block i+1 minus that of block i,
@@ -376,7 +406,11 @@ def run_ours(args, cfg, rank, world, local_rank):
     # step roofline: slower of offloaded bytes at the measured
     # host link and algorithmic GEMM FLOPs at the bf16 tensor peak
     flops_step = 2 * (nb * (24.0 * T * d * d + 4.0 * B * S * S * d) + 2.0 * T * d * V)
-    t_link = wire_per_dir / (h2d_gbs * 1e9) if h2d_gbs else None
+    probe_up, probe_dn = link_probe(dev)
+    # full duplex: the slower direction binds; the link capability is the better
+    # of the probe and what the step's own block copies reached
+    link_gbs = max(min(probe_up, probe_dn), min(h2d_gbs or 0.0, d2h_gbs or 0.0))
+    t_link = wire_per_dir / (link_gbs * 1e9)
     split = cfg["arith"] == "f32"
     # f32-faithful GEMMs run 3 bf16 tensor passes per algorithmic FLOP
     # (hi*hi + hi*lo + lo*hi): their peak is the bf16 dense peak / 3
@@ -425,7 +459,10 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "k2_ms_per_step": k2_ms / args.steps,
                      "k2_gdraws_per_s": (k2_draws / (k2_ms * 1e-3) / 1e9) if k2_ms else None},
         "step_roofline": {"bound": "pcie" if (t_link or 0) >= t_tensor else "tensor",
-                          "h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs,
+                          "link_probe_gbs": {"h2d": probe_up, "d2h": probe_dn,
+                                             "note": "1 GiB pinned copies, both directions "
+                                                     "at once, best of 3"},
+                          "h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs, "link_gbs_used": link_gbs,
                           "bytes_per_dir": wire_per_dir, "t_link_ms": (t_link or 0) * 1e3,
                           "t_tensor_ms": t_tensor * 1e3, "frac": t_roof / step_s,
                           "tensor_note": "algorithmic dual-forward FLOPs (scheduler.py:288-295 "
