@@ -33,6 +33,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 CONFIGS = {
+    # the reference's own CPU-runnable case: MeZO, every block resident in HBM
+    "cfg1": dict(workload="OPT-125M ZO-SGD (MeZO) fp32, batch 16 x seq 128, no offload",
+                 spec=(12, 768, 12, 50272, 128), B=16, arith="f32", codec="none", lr=1e-6,
+                 slots=3, resident=True),
     "cfg2": dict(workload="OPT-1.3B ZO2 per-block offload fp32, batch 16 x seq 512",
                  spec=(24, 2048, 32, 50272, 512), B=16, arith="f32", codec="none", lr=1e-7,
                  slots=3),
@@ -315,8 +319,12 @@ def run_ours(args, cfg, rank, world, local_rank):
                                  host_masters=shm)
     else:
         params = init_params(spec, RngState(SEED), device=dev, codec=cfg["codec"])
-    rt = OffloadRuntime(params, k_slots=cfg["slots"], codec=cfg["codec"],
-                        capacity_bytes=cfg.get("cap", float("inf")), device=dev)
+    if cfg.get("resident"):  # MeZO: blocks live in HBM, transfers are no-ops
+        from paper_2503_12668_b200.runtime import ResidentRuntime
+        rt = ResidentRuntime(params, device=dev)
+    else:
+        rt = OffloadRuntime(params, k_slots=cfg["slots"], codec=cfg["codec"],
+                            capacity_bytes=cfg.get("cap", float("inf")), device=dev)
     eng = Zo2Engine(TransformerWorkload(params, cfg["arith"]),
                     ZOConfig(EPS, cfg["lr"], max(1, args.steps), SEED), rt, validate=True,
                     operand_sets=args.operand_sets, rng=args.rng)
@@ -385,6 +393,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     # with sharded transfers; the upload event also covers the NVLink all-gather)
     h2d_gbs = (sum(rt.wire_nbytes for _ in up) / sum(e.duration for e in up) / 1e9) if up else None
     d2h_gbs = (sum(rt.wire_nbytes for _ in off) / sum(e.duration for e in off) / 1e9) if off else None
+    if cfg.get("resident"):
+        h2d_gbs = d2h_gbs = None  # no weight traffic
     comp_busy = sum(tl.lane_busy(Lane.COMPUTE) for tl in tls)
     idle_pct = max(0.0, 100.0 * (1.0 - comp_busy / (dev_ms * 1e-3))) if tls else None
 
@@ -402,7 +412,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     tokens_step = T * world
     value = tokens_step * args.steps / (ms * 1e-3)
     e2e_value = tokens_step * args.steps / e2e_s
-    wire_per_dir = nb * rt.wire_nbytes
+    wire_per_dir = 0 if cfg.get("resident") else nb * rt.wire_nbytes
     # step roofline: slower of offloaded bytes at the measured
     # host link and algorithmic GEMM FLOPs at the bf16 tensor peak
     flops_step = 2 * (nb * (24.0 * T * d * d + 4.0 * B * S * S * d) + 2.0 * T * d * V)
@@ -410,7 +420,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     # full duplex: the slower direction binds; the link capability is the better
     # of the probe and what the step's own block copies reached
     link_gbs = max(min(probe_up, probe_dn), min(h2d_gbs or 0.0, d2h_gbs or 0.0))
-    t_link = wire_per_dir / (link_gbs * 1e9)
+    t_link = wire_per_dir / (link_gbs * 1e9) if link_gbs else 0.0
     split = cfg["arith"] == "f32"
     # f32-faithful GEMMs run 3 bf16 tensor passes per algorithmic FLOP
     # (hi*hi + hi*lo + lo*hi): their peak is the bf16 dense peak / 3
