@@ -7,7 +7,6 @@
 // vectors, grids are sized in multiples of the 148 SMs.
 #include "zo2_common.cuh"
 #include "zo2_rng.h"
-#include "zo2_zgen.cuh"
 #include "zo2_rng_fast.h"
 #include <atomic>
 #include <string.h>

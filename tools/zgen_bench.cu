@@ -1,7 +1,7 @@
 // Microbenchmark of the exact z generator pieces (tools only).
 #include <cstdio>
 #include <cuda_runtime.h>
-#include "../paper_2503_12668_b200/csrc/zo2_zgen.cuh"
+#include "zgen_warp.cuh"
 
 __global__ void k_philox(uint64_t n_blocks, uint64_t seed, uint64_t *sink) {
   uint64_t acc = 0;

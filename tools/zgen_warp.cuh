@@ -1,4 +1,5 @@
-// zo2_zgen.cuh -- warp-cooperative evaluation of z = ndtri(u) (device only).
+// zgen_warp.cuh -- (tools only) the previous, warp-cooperative evaluation of
+// z = ndtri(u), kept for A/B against the CTA-queue kernel in zo2_k2.cu.
 //
 // Cephes ndtri has a cheap central branch (73% of draws) and an expensive tail
 // branch (2 logs, sqrt, 2 divisions, degree-8 rationals).  Evaluated per lane,
@@ -9,7 +10,7 @@
 // (same scalar routines, same operation order) -- only the lane that computes
 // a given draw changes.
 #pragma once
-#include "zo2_rng.h"
+#include "../paper_2503_12668_b200/csrc/zo2_rng.h"
 #ifndef ZO2_CENTRAL_BRANCHLESS
 #define ZO2_CENTRAL_BRANCHLESS 0
 #endif
