@@ -165,11 +165,155 @@ __global__ void __launch_bounds__(NT) k_layernorm(const float *x, uint32_t dim,
   }
 }
 
+// Warp per row for dim % 128 == 0 and dim <= 4096: each lane holds V4 float4
+// chunks (16-byte loads, chunk i at column 4 * (32 i + lane)), the two
+// reductions are warp shuffles (no CTA barriers), and the bf16 hi / lo planes
+// go out as 8-byte stores.  Same f64 accumulation as k_layernorm.
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <int V4>
+__global__ void __launch_bounds__(256) k_layernorm_warp(const float *x, uint64_t rows,
+                                                        uint32_t dim, const float *gamma,
+                                                        const float *beta,
+                                                        __nv_bfloat16 *out_hi,
+                                                        __nv_bfloat16 *out_lo) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t row = (uint64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const float4 *xr = (const float4 *)(x + row * dim);
+  float4 v[V4];
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    v[i] = xr[i * 32 + lane];
+    s += (double)v[i].x + (double)v[i].y + (double)v[i].z + (double)v[i].w;
+  }
+  const float mu = (float)(warp_sum_d(s) / dim);
+  double q = 0.0;
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    const float a = v[i].x - mu, b = v[i].y - mu, c = v[i].z - mu, e = v[i].w - mu;
+    q += (double)a * a + (double)b * b + (double)c * c + (double)e * e;
+  }
+  const float var = (float)(warp_sum_d(q) / dim);
+  const float inv = 1.0f / sqrtf(var + 1e-5f);
+  const float4 *g4 = (const float4 *)gamma, *b4 = (const float4 *)beta;
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    const int c4 = i * 32 + lane;
+    const float4 g = g4[c4], b = b4[c4];
+    const float y0 = (v[i].x - mu) * inv * g.x + b.x, y1 = (v[i].y - mu) * inv * g.y + b.y;
+    const float y2 = (v[i].z - mu) * inv * g.z + b.z, y3 = (v[i].w - mu) * inv * g.w + b.w;
+    const __nv_bfloat162 h01 = __floats2bfloat162_rn(y0, y1), h23 = __floats2bfloat162_rn(y2, y3);
+    uint2 hv;
+    hv.x = *reinterpret_cast<const uint32_t *>(&h01);
+    hv.y = *reinterpret_cast<const uint32_t *>(&h23);
+    *(uint2 *)(out_hi + row * dim + 4 * (uint64_t)c4) = hv;
+    if (out_lo) {
+      const __nv_bfloat162 l01 = __floats2bfloat162_rn(y0 - __low2float(h01), y1 - __high2float(h01));
+      const __nv_bfloat162 l23 = __floats2bfloat162_rn(y2 - __low2float(h23), y3 - __high2float(h23));
+      uint2 lv;
+      lv.x = *reinterpret_cast<const uint32_t *>(&l01);
+      lv.y = *reinterpret_cast<const uint32_t *>(&l23);
+      *(uint2 *)(out_lo + row * dim + 4 * (uint64_t)c4) = lv;
+    }
+  }
+}
+
+// One 256-thread CTA per row for dim % 1024 == 0 (OPT widths 2048 .. 12288):
+// each thread holds V float4 chunks (chunk i at column 4 * (256 i + t)), sum and
+// sum of squares go through ONE f64 block reduction (var = E[x^2] - mu^2 in
+// f64: exact enough for f32 data with |mean| << 2^20 std), 8-byte bf16 stores.
+template <int V>
+__global__ void __launch_bounds__(256) k_layernorm_cta(const float *x, uint32_t dim,
+                                                       const float *gamma, const float *beta,
+                                                       __nv_bfloat16 *out_hi,
+                                                       __nv_bfloat16 *out_lo) {
+  __shared__ double2 part[8];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint64_t row = blockIdx.x;
+  const float4 *xr = (const float4 *)(x + row * dim);
+  float4 v[V];
+  double s = 0.0, q = 0.0;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    v[i] = xr[i * 256 + t];
+    const double a = v[i].x, b = v[i].y, c = v[i].z, e = v[i].w;
+    s += a + b + c + e;
+    q += a * a + b * b + c * c + e * e;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    q += __shfl_xor_sync(0xffffffffu, q, o);
+  }
+  if (lane == 0) part[warp] = make_double2(s, q);
+  __syncthreads();
+  double ss = 0.0, qq = 0.0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    ss += part[w].x;
+    qq += part[w].y;
+  }
+  const double mud = ss / dim;
+  const float mu = (float)mud;
+  const float var = (float)(qq / dim - mud * mud);
+  const float inv = 1.0f / sqrtf(var + 1e-5f);
+  const float4 *g4 = (const float4 *)gamma, *b4 = (const float4 *)beta;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const int c4 = i * 256 + t;
+    const float4 g = g4[c4], b = b4[c4];
+    const float y0 = (v[i].x - mu) * inv * g.x + b.x, y1 = (v[i].y - mu) * inv * g.y + b.y;
+    const float y2 = (v[i].z - mu) * inv * g.z + b.z, y3 = (v[i].w - mu) * inv * g.w + b.w;
+    const __nv_bfloat162 h01 = __floats2bfloat162_rn(y0, y1), h23 = __floats2bfloat162_rn(y2, y3);
+    uint2 hv;
+    hv.x = *reinterpret_cast<const uint32_t *>(&h01);
+    hv.y = *reinterpret_cast<const uint32_t *>(&h23);
+    *(uint2 *)(out_hi + row * dim + 4 * (uint64_t)c4) = hv;
+    if (out_lo) {
+      const __nv_bfloat162 l01 = __floats2bfloat162_rn(y0 - __low2float(h01), y1 - __high2float(h01));
+      const __nv_bfloat162 l23 = __floats2bfloat162_rn(y2 - __low2float(h23), y3 - __high2float(h23));
+      uint2 lv;
+      lv.x = *reinterpret_cast<const uint32_t *>(&l01);
+      lv.y = *reinterpret_cast<const uint32_t *>(&l23);
+      *(uint2 *)(out_lo + row * dim + 4 * (uint64_t)c4) = lv;
+    }
+  }
+}
+
 extern "C" int zo2_layernorm(const float *x, uint64_t rows, uint32_t dim, const float *gamma,
                              const float *beta, void *out_hi, void *out_lo, void *cs) {
   if (rows == 0) return ZO2_OK;
   __nv_bfloat16 *hi = (__nv_bfloat16 *)out_hi, *lo = (__nv_bfloat16 *)out_lo;
-  if (dim <= 256 * 8)
+  const unsigned wg = (unsigned)((rows + 7) / 8);
+  const bool al = ((uintptr_t)x % 16 == 0) && ((uintptr_t)gamma % 16 == 0) &&
+                  ((uintptr_t)beta % 16 == 0) && ((uintptr_t)out_hi % 8 == 0) &&
+                  ((uintptr_t)out_lo % 8 == 0);
+  if (al && dim % 1024 == 0 && dim <= 16 * 1024) {
+    switch (dim / 1024) {
+#define ZO2_LNC(n) case n: k_layernorm_cta<n><<<(unsigned)rows, 256, 0, S(cs)>>>(x, dim, gamma, beta, hi, lo); break;
+      ZO2_LNC(1) ZO2_LNC(2) ZO2_LNC(3) ZO2_LNC(4) ZO2_LNC(5) ZO2_LNC(6) ZO2_LNC(7) ZO2_LNC(8)
+      ZO2_LNC(9) ZO2_LNC(10) ZO2_LNC(11) ZO2_LNC(12) ZO2_LNC(13) ZO2_LNC(14) ZO2_LNC(15)
+      ZO2_LNC(16)
+#undef ZO2_LNC
+      default: break;
+    }
+  } else if (al && dim % 128 == 0 && dim <= 2048) {
+    switch (dim / 128) {
+#define ZO2_LNW(n) case n: k_layernorm_warp<n><<<wg, 256, 0, S(cs)>>>(x, rows, dim, gamma, beta, hi, lo); break;
+      ZO2_LNW(1) ZO2_LNW(2) ZO2_LNW(3) ZO2_LNW(4) ZO2_LNW(5) ZO2_LNW(6) ZO2_LNW(7) ZO2_LNW(8)
+      ZO2_LNW(9) ZO2_LNW(10) ZO2_LNW(11) ZO2_LNW(12) ZO2_LNW(13) ZO2_LNW(14) ZO2_LNW(15)
+      ZO2_LNW(16) ZO2_LNW(17) ZO2_LNW(18) ZO2_LNW(19) ZO2_LNW(20) ZO2_LNW(21) ZO2_LNW(22)
+      ZO2_LNW(23) ZO2_LNW(24) ZO2_LNW(25) ZO2_LNW(26) ZO2_LNW(27) ZO2_LNW(28) ZO2_LNW(29)
+      ZO2_LNW(30) ZO2_LNW(31) ZO2_LNW(32)
+#undef ZO2_LNW
+      default: break;
+    }
+  } else if (dim <= 256 * 8)
     k_layernorm<256, 8><<<(unsigned)rows, 256, 0, S(cs)>>>(x, dim, gamma, beta, hi, lo);
   else if (dim <= 256 * 24)
     k_layernorm<256, 24><<<(unsigned)rows, 256, 0, S(cs)>>>(x, dim, gamma, beta, hi, lo);

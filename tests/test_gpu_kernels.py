@@ -375,7 +375,7 @@ def test_gemm_cross_entropy(cuda, gemm_variant, split):
 
 
 # ------------------------------------------------------------------ LN / attention / embed
-@pytest.mark.parametrize("dim", [32, 768, 2048, 7168])
+@pytest.mark.parametrize("dim", [32, 768, 2048, 4096, 7168, 12288])
 def test_layernorm(cuda, dim):
     rows = 64
     x = torch.randn(rows, dim, device=cuda) * 3 + 1
