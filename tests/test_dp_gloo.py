@@ -3,6 +3,7 @@ on CPU): batch sharding + the loss-sum all-reduce reproduce the single-process
 global-batch losses and g.  The per-rank forward here is the
 CPU oracle (test infrastructure); on B200 the same helpers run with NCCL."""
 import os
+import tempfile
 
 import numpy as np
 import pytest
@@ -11,9 +12,9 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 
-def _worker(rank, world, port, out):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+def _worker(rank, world, store, out):
+    # file rendezvous: no fixed TCP port that another job could hold
+    dist.init_process_group("gloo", init_method=f"file://{store}", rank=rank, world_size=world)
     from oracle import zo2_oracle as O
     from paper_2503_12668_b200.parallel import (allreduce_loss_sums, projected_gradient,
                                                 shard_indices)
@@ -44,10 +45,17 @@ def _worker(rank, world, port, out):
 @pytest.mark.timeout(300)
 def test_two_rank_gloo_matches_global_batch():
     from oracle import zo2_oracle as O
-    world, port = 2, 29531
+    world = 2
+    fd, store = tempfile.mkstemp(prefix="zo2_gloo_store_")
+    os.close(fd)
+    os.unlink(store)
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+    try:
+        mp.spawn(_worker, args=(world, store, out), nprocs=world, join=True)
+    finally:
+        if os.path.exists(store):
+            os.unlink(store)
     assert out[0] == out[1]                      # every rank forms the same g
     spec = O.Spec(2, 32, 4, 64, 16)
     tok, tgt = O.gen_synthetic(spec.vocab, spec.seq_len, 32, 3)

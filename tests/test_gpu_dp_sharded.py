@@ -4,7 +4,7 @@ two ranks (gloo, sharing one GPU) must produce exactly what two ranks with
 private masters and full-block transfers produce -- same losses, same g,
 bit-identical final parameters -- while each moves half the PCIe bytes."""
 import os
-import socket
+import tempfile
 
 import numpy as np
 import pytest
@@ -14,21 +14,15 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 
-def _free_port():
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        return s.getsockname()[1]
-
-
-def _worker(rank, world, port, sharded, codec, q):
+def _worker(rank, world, store, sharded, codec, q):
     try:
-        q.put((rank, _body(rank, world, port, sharded, codec)))
+        q.put((rank, _body(rank, world, store, sharded, codec)))
     except Exception as e:  # surface the failure instead of a queue timeout
         import traceback
         q.put((rank, {"error": f"{e!r}\n{traceback.format_exc()}"}))
 
 
-def _body(rank, world, port, sharded, codec):
+def _body(rank, world, store, sharded, codec):
     import torch.distributed as dist
     from paper_2503_12668_b200.data import gen_synthetic
     from paper_2503_12668_b200.engine import TransformerWorkload, ZOConfig, Zo2Engine
@@ -38,13 +32,14 @@ def _body(rank, world, port, sharded, codec):
     from paper_2503_12668_b200.runtime import (_TORCH_STORAGE, OffloadRuntime,
                                                SharedHostMasters, init_params, params_digest)
     torch.cuda.set_device(0)
-    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+    # file rendezvous: no TCP port to race for between the probe and the bind
+    dist.init_process_group("gloo", init_method=f"file://{store}", rank=rank,
                             world_size=world)
     spec = ModelSpec(3, 64, 4, 128, 32)
     seed, steps, B = 11, 3, 2
     shm = None
     if sharded:
-        name = [f"zo2_test_{port}" if rank == 0 else None]
+        name = [f"zo2_test_{os.path.basename(store)}" if rank == 0 else None]
         dist.broadcast_object_list(name, src=0)
         sdt = _TORCH_STORAGE[CODEC_FORMATS[codec] if codec else ElemFormat.F32]
         n = module_size(spec, block_id(0))
@@ -78,8 +73,10 @@ def _body(rank, world, port, sharded, codec):
 def _run(sharded, codec=None):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, sharded, codec, q)) for r in range(2)]
+    fd, store = tempfile.mkstemp(prefix="zo2_dp_store_")
+    os.close(fd)
+    os.unlink(store)  # the FileStore creates it
+    ps = [ctx.Process(target=_worker, args=(r, 2, store, sharded, codec, q)) for r in range(2)]
     for p in ps:
         p.start()
     try:
@@ -89,6 +86,8 @@ def _run(sharded, codec=None):
             p.join(timeout=60)
             if p.is_alive():
                 p.kill()
+        if os.path.exists(store):
+            os.unlink(store)
     for r, out in res.items():
         assert "error" not in out, f"rank {r}: {out['error']}"
     return res
