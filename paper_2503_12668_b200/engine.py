@@ -219,7 +219,7 @@ class Zo2Engine:
     def __init__(self, workload: TransformerWorkload, cfg: ZOConfig, runtime: OffloadRuntime,
                  *, overlap: bool = True, backend: str = "cuda", update_mode: str = "deferred",
                  cost=None, trace=None, validate: bool = True, prepare_lane: bool = True,
-                 operand_sets: int = 2, rng: str = "exact"):
+                 operand_sets: int = 1, rng: str = "exact"):
         if update_mode not in ("deferred", "naive"):
             raise ValueError(f"unknown update_mode {update_mode!r}")
         if rng not in RNG_MODES:

@@ -199,7 +199,7 @@ class DualForward:
     """HBM working set + kernel sequence for the dual forward of one engine."""
 
     def __init__(self, spec: ModelSpec, batch_size: int, arith: str, device,
-                 operand_sets: int = 2):
+                 operand_sets: int = 1):
         if arith not in ("f32", "bf16"):
             raise ValueError(f"device forward supports arith f32 (3-pass bf16 split) or bf16, "
                              f"got {arith!r}")
