@@ -854,32 +854,61 @@ struct AttnTcCfg {
   static constexpr int QTILE = ATT_Q * 128;              // one 128-row panel, bytes
   static constexpr int KTILE = ATT_K * 128;              // one 64-row panel
   static constexpr int KV = PL * PAN * KTILE;            // K (or V) tile, all planes
-  static constexpr int PB = PL * QTILE;                  // P [128 q x 64 keys], all planes
-  static constexpr int NS = 3;                           // K/V ring stages
+  static constexpr int NS = 2;                           // K/V ring stages
   static constexpr int Q_OFF = 0;
   static constexpr int KV_OFF = Q_OFF + PL * PAN * QTILE;  // stage s: K at +2s*KV, V at +(2s+1)*KV
-  static constexpr int P_OFF = KV_OFF + NS * 2 * KV;       // 2 P buffers
-  static constexpr int BAR_OFF = P_OFF + 2 * PB;
+  static constexpr int BAR_OFF = KV_OFF + NS * 2 * KV;
   static constexpr int SMEM = BAR_OFF + 256 + 4 * 128 * 4 + 1024;
-  static constexpr uint32_t TMEM_COLS = 256;             // S 2 x 64 + O hd (<= 128)
+  // TMEM columns (256 per CTA, two CTAs per SM): S buffers, O, P (bf16 pairs)
+  static constexpr int SB = (HD + (SPLIT ? 64 : 32) + 2 * ATT_K <= 256) ? 2 : 1;
+  static constexpr uint32_t T_O = SB * ATT_K;
+  static constexpr uint32_t T_P = T_O + HD;               // P hi: 32 columns (64 keys)
+  static constexpr uint32_t T_PLO = T_P + ATT_K / 2;      // P lo (split)
+  static constexpr uint32_t TMEM_COLS = 256;
+  static_assert(T_PLO + (SPLIT ? ATT_K / 2 : 0) <= TMEM_COLS, "TMEM budget");
 };
+
+__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 lanes x 16 consecutive 32-bit columns from 16 registers per thread
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15])
+      : "memory");
+}
 
 // 8 softmax warps (warp w and w + 4 share TMEM lane quadrant w % 4 = 32 query
 // rows and split the 64 columns of S and the hd columns of O) + 1 warp that
-// issues TMA and tcgen05.mma; the two sides meet only on mbarriers.
+// issues TMA and tcgen05.mma; the two sides meet only on mbarriers.  P goes
+// to TMEM (tcgen05.st) and is the A operand of P.V straight from there, so
+// a CTA needs no P staging in shared memory: two CTAs per SM.
 constexpr int ATT_SOFT = 256;
 template <int HD, bool SPLIT>
-__global__ void __launch_bounds__(ATT_SOFT + 32, 1) k_attn_tc(const __grid_constant__ AttnTcArgs a) {
+__global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_constant__ AttnTcArgs a) {
   using C = AttnTcCfg<HD, SPLIT>;
-  constexpr int NS = C::NS;
+  constexpr int NS = C::NS, SB = C::SB;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t *bar_kv = (uint64_t *)(smem + C::BAR_OFF);  // [NS] tile loaded (TMA)
-  uint64_t *bar_s = bar_kv + NS;                       // [2]  S written (MMA commit)
-  uint64_t *bar_sfree = bar_s + 2;                     // [2]  S read (256 arrivals)
-  uint64_t *bar_p = bar_sfree + 2;                     // [2]  P written (256 arrivals)
-  uint64_t *bar_o = bar_p + 2;                         // [2]  P.V done (MMA commit)
-  uint32_t *tmem_slot = (uint32_t *)(bar_o + 2);
+  uint64_t *bar_s = bar_kv + NS;                       // [SB] S written (MMA commit)
+  uint64_t *bar_sfree = bar_s + 2;                     // [SB] S read (256 arrivals)
+  uint64_t *bar_p = bar_sfree + 2;                     // P written to TMEM (256 arrivals)
+  uint64_t *bar_o = bar_p + 1;                         // P.V done (MMA commit)
+  uint64_t *bar_kvfree = bar_o + 1;                    // [NS] ring stage read by its MMAs
+  uint32_t *tmem_slot = (uint32_t *)(bar_kvfree + NS);
   float *xch = (float *)(smem + C::BAR_OFF + 256);     // [2][128] row max, then [2][128] row sum
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // heavy (late) query tiles first
@@ -891,12 +920,13 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 1) k_attn_tc(const __grid_const
 
   if (threadIdx.x == ATT_SOFT) {
     for (int i = 0; i < NS; ++i) mbar_init(&bar_kv[i], 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < SB; ++i) {
       mbar_init(&bar_s[i], 1);
       mbar_init(&bar_sfree[i], ATT_SOFT);
-      mbar_init(&bar_p[i], ATT_SOFT);
-      mbar_init(&bar_o[i], 1);
     }
+    mbar_init(bar_p, ATT_SOFT);
+    mbar_init(bar_o, 1);
+    for (int i = 0; i < NS; ++i) mbar_init(&bar_kvfree[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int p = 0; p < C::PL; ++p) {
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tq[p]) : "memory");
@@ -913,13 +943,12 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 1) k_attn_tc(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_o = tmem + 128;
+  const uint32_t t_o = tmem + C::T_O;
 
   if (warp == ATT_SOFT / 32) {
     // ================================================ TMA + MMA issue (one thread)
     if (lane == 0) {
-      const uint32_t sq = smem_u32(smem + C::Q_OFF), skv = smem_u32(smem + C::KV_OFF),
-                     sp = smem_u32(smem + C::P_OFF);
+      const uint32_t sq = smem_u32(smem + C::Q_OFF), skv = smem_u32(smem + C::KV_OFF);
       auto load_tile = [&](uint32_t g) {
         const uint32_t j = g < n_kt ? g : g - n_kt;
         const bool with_v = g >= n_kt, with_q = g == 0;
@@ -945,10 +974,10 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 1) k_attn_tc(const __grid_const
                           (int)(2 * d + h * HD + 64 * c), krow);
           }
       };
-      // S[g & 1] = Q K(g)^T (3 passes split); K-major A and B
+      // S[g % SB] = Q K(g)^T (3 passes split in pass 2); K-major A and B
       auto issue_qk = [&](uint32_t g) {
         constexpr uint32_t id = idesc_bf16_b(ATT_K, false);
-        const uint32_t ts = tmem + (g & 1u) * ATT_K;
+        const uint32_t ts = tmem + (g % SB) * ATT_K;
         const uint32_t sk = skv + (uint32_t)(2 * (int)(g % NS) * C::KV);
         for (int ks = 0; ks < HD / 16; ++ks) {
           const uint32_t qo = (uint32_t)((ks / 4) * C::QTILE + (ks % 4) * 32);
@@ -960,60 +989,56 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 1) k_attn_tc(const __grid_const
             tc_mma(ts, sw128_desc(sq + C::PAN * C::QTILE + qo), kd, id, 1u);
           }
         }
-        tc_commit(&bar_s[g & 1u]);
+        tc_commit(&bar_s[g % SB]);
       };
-      // O += P(j) V(j): A = P [128 q x 64 keys] K-major, B = V [64 keys x hd] MN-major
+      // O += P(j) V(j): A = P [128 q x 64 keys] in TMEM, B = V [64 keys x hd] MN-major
       auto issue_pv = [&](uint32_t g) {
-        const uint32_t j = g - n_kt, pb = j & 1u;
+        const uint32_t j = g - n_kt;
         constexpr uint32_t id = idesc_bf16_b(HD, true);
         constexpr uint32_t vlbo = (uint32_t)C::KTILE;  // next 64 hd columns: next panel
         const uint32_t sv = skv + (uint32_t)((2 * (int)(g % NS) + 1) * C::KV);
-        const uint32_t spb = sp + pb * (uint32_t)C::PB;
         for (int ks = 0; ks < ATT_K / 16; ++ks) {
-          const uint32_t poff = (uint32_t)(ks * 32);
           const uint32_t voff = (uint32_t)(ks * 16 * 128);  // 16 keys x 128 B
-          const uint64_t pa = sw128_desc(spb + poff), vb = sw128_desc_mn(sv + voff, vlbo);
-          tc_mma(t_o, pa, vb, id, (j | (uint32_t)ks) != 0);
+          const uint32_t pa = tmem + C::T_P + (uint32_t)(ks * 8);  // 16 keys = 8 columns
+          const uint64_t vb = sw128_desc_mn(sv + voff, vlbo);
+          tc_mma_ts(t_o, pa, vb, id, (j | (uint32_t)ks) != 0);
           if (SPLIT) {
-            tc_mma(t_o, pa, sw128_desc_mn(sv + C::PAN * C::KTILE + voff, vlbo), id, 1u);
-            tc_mma(t_o, sw128_desc(spb + C::QTILE + poff), vb, id, 1u);
+            tc_mma_ts(t_o, pa, sw128_desc_mn(sv + C::PAN * C::KTILE + voff, vlbo), id, 1u);
+            tc_mma_ts(t_o, tmem + C::T_PLO + (uint32_t)(ks * 8), vb, id, 1u);
           }
         }
-        tc_commit(&bar_o[pb]);
+        tc_commit(bar_o);
       };
 
       for (uint32_t g = 0; g < (uint32_t)NS && g < n_all; ++g) load_tile(g);
       mbar_wait(&bar_kv[0], 0);
       tc_fence_after();
       issue_qk(0);
+      if (n_kt > 0) tc_commit(&bar_kvfree[0]);
       for (uint32_t g = 0; g < n_all; ++g) {
-        // refill the ring stage of tile g - 1 (consumed by S(g - 1) / P.V(g - 1)).
-        // Done before S(g + 1) is issued: S(g + 1) shares bar_s with S(g - 1),
-        // and a parity wait must never trail its barrier by two phases.
+        // refill the ring stage of tile g - 1 (consumed by S(g - 1) / P.V(g - 1))
         if (g >= 1 && g - 1 + NS < n_all) {
           const uint32_t gp = g - 1;
-          if (gp >= n_kt) {
-            const uint32_t jp = gp - n_kt;
-            mbar_wait(&bar_o[jp & 1u], (jp >> 1) & 1u);
-          } else {
-            mbar_wait(&bar_s[gp & 1u], (gp >> 1) & 1u);
-          }
+          // a barrier per ring stage (committed after the last MMA reading it):
+          // its next phase belongs to tile gp + NS, loaded right here
+          mbar_wait(&bar_kvfree[gp % NS], (gp / NS) & 1u);
           load_tile(gp + NS);
         }
-        // S(g + 1) next, so it runs while the softmax warps work on S(g):
-        // needs K(g + 1) and the S buffer of tile g - 1 drained
+        // S(g + 1) next: needs K(g + 1) and its S buffer drained (tile g + 1 - SB)
         if (g + 1 < n_all) {
           const uint32_t gn = g + 1;
           mbar_wait(&bar_kv[gn % NS], (gn / NS) & 1u);
-          if (gn >= 2) mbar_wait(&bar_sfree[gn & 1u], ((gn - 2) >> 1) & 1u);
+          if (gn >= (uint32_t)SB) mbar_wait(&bar_sfree[gn % SB], ((gn - SB) / SB) & 1u);
           tc_fence_after();
           issue_qk(gn);
+          if (gn < n_kt) tc_commit(&bar_kvfree[gn % NS]);  // pass 1: K read by S only
         }
-        if (g >= n_kt) {  // P.V of this tile once the softmax wrote P(j)
+        if (g >= n_kt) {  // P.V of this tile once the softmax stored P(j)
           const uint32_t j = g - n_kt;
-          mbar_wait(&bar_p[j & 1u], (j >> 1) & 1u);
+          mbar_wait(bar_p, j & 1u);
           tc_fence_after();
           issue_pv(g);
+          tc_commit(&bar_kvfree[g % NS]);
         }
       }
     }
@@ -1028,12 +1053,12 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 1) k_attn_tc(const __grid_const
       const bool pass2 = g >= n_kt;
       const uint32_t j = pass2 ? g - n_kt : g;
       const int lim = (int)(qt * ATT_Q) + r - (int)(j * ATT_K) - c0;  // visible: i <= lim
-      mbar_wait(&bar_s[g & 1u], (g >> 1) & 1u);
+      mbar_wait(&bar_s[g % SB], (g / SB) & 1u);
       tc_fence_after();
       uint32_t v[32];
-      tmem_ld32(tmem + (g & 1u) * ATT_K + lane_base + (uint32_t)c0, v);
+      tmem_ld32(tmem + (g % SB) * ATT_K + lane_base + (uint32_t)c0, v);
       tc_fence_before();
-      mbar_arrive(&bar_sfree[g & 1u]);
+      mbar_arrive(&bar_sfree[g % SB]);
       if (!pass2) {
 #pragma unroll
         for (int i = 0; i < 32; ++i)
@@ -1045,10 +1070,6 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 1) k_attn_tc(const __grid_const
         }
         continue;
       }
-      // P(j) -> smem buffer j & 1 once P.V(j - 2) released it
-      const uint32_t pb = j & 1u;
-      if (j >= 2) mbar_wait(&bar_o[pb], ((j - 2) >> 1) & 1u);
-      uint8_t *prow = smem + C::P_OFF + pb * C::PB + (r >> 3) * 1024 + (r & 7) * 128;
       float pv[32];
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
@@ -1056,36 +1077,32 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 1) k_attn_tc(const __grid_const
         pv[i] = e;
         lsum += e;
       }
-      const int kc = c0 >> 3;  // first 16-byte chunk of these 32 keys
+      uint32_t hi[16], lo[16];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint32_t hi[4], lo[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float x0 = pv[8 * q + 2 * e], x1 = pv[8 * q + 2 * e + 1];
-          const __nv_bfloat162 hv = __floats2bfloat162_rn(x0, x1);
-          hi[e] = *reinterpret_cast<const uint32_t *>(&hv);
-          if (SPLIT) {
-            const __nv_bfloat162 lv = __floats2bfloat162_rn(x0 - __low2float(hv),
-                                                            x1 - __high2float(hv));
-            lo[e] = *reinterpret_cast<const uint32_t *>(&lv);
-          }
+      for (int e = 0; e < 16; ++e) {
+        const __nv_bfloat162 hv = __floats2bfloat162_rn(pv[2 * e], pv[2 * e + 1]);
+        hi[e] = *reinterpret_cast<const uint32_t *>(&hv);
+        if (SPLIT) {
+          const __nv_bfloat162 lv = __floats2bfloat162_rn(pv[2 * e] - __low2float(hv),
+                                                          pv[2 * e + 1] - __high2float(hv));
+          lo[e] = *reinterpret_cast<const uint32_t *>(&lv);
         }
-        const int chunk = (kc + q) ^ (r & 7);
-        *(uint4 *)(prow + chunk * 16) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        if (SPLIT)
-          *(uint4 *)(prow + C::QTILE + chunk * 16) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&bar_p[pb]);
+      // P(j) replaces P(j - 1) in TMEM once P.V(j - 1) has read it
+      if (j >= 1) {
+        mbar_wait(bar_o, (j - 1) & 1u);
+        tc_fence_after();
+      }
+      tmem_st16(tmem + C::T_P + lane_base + (uint32_t)(c0 / 2), hi);
+      if (SPLIT) tmem_st16(tmem + C::T_PLO + lane_base + (uint32_t)(c0 / 2), lo);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(bar_p);
     }
     // ---------------------------------------------- epilogue: O / l -> bf16 planes
     xch[256 + half * 128 + r] = lsum;
-    {
-      const uint32_t jl = n_kt - 1;
-      mbar_wait(&bar_o[jl & 1u], (jl >> 1) & 1u);  // last P.V (and so every P.V) done
-      tc_fence_after();
-    }
+    mbar_wait(bar_o, (n_kt - 1) & 1u);  // last P.V (and so every P.V) done
+    tc_fence_after();
     asm volatile("bar.sync 1, %0;" ::"n"(ATT_SOFT) : "memory");
     const float inv = 1.0f / (xch[256 + r] + xch[384 + r]);
     __nv_bfloat16 *oh = a.out_hi + (uint64_t)(row0 + r) * d + h * HD;
