@@ -331,19 +331,36 @@ class OffloadRuntime:
         # other, never behind the compute lane's loss all-reduce
         g = dist.new_group(list(range(world))) if group is None else group
         self.shard = (rank, world, g, rank * n, (rank + 1) * n)
-        return True
+        # self-test of the in-place all-gather this path relies on; any
+        # backend refusal falls back to replicated full-block transfers
+        try:
+            probe = torch.full((4 * world,), 0, dtype=torch.uint8, device=self.device)
+            probe[4 * rank:4 * rank + 4] = rank + 1
+            self._gather_bytes(probe, 4, g)
+            torch.cuda.synchronize(self.device)
+            want = torch.arange(1, world + 1, device=self.device,
+                                dtype=torch.uint8).repeat_interleave(4)
+            ok = bool(torch.equal(probe, want))
+        except Exception:  # noqa: BLE001 -- any failure means: do not shard
+            ok = False
+        if not ok:
+            self.shard = None
+        return ok
 
-    def _gather(self, slot: int) -> None:
+    def _gather_bytes(self, full: torch.Tensor, chunk: int, g) -> None:
         import torch.distributed as dist
-        rank, world, g, lo, hi = self.shard
-        full = self.slots[slot].view(torch.uint8)
-        esize = self.slots[slot].element_size()
-        mine = full[lo * esize:hi * esize]
+        rank, world = self.shard[0], self.shard[1]
+        mine = full[rank * chunk:(rank + 1) * chunk]
         if dist.get_backend(g) == "nccl":
             dist.all_gather_into_tensor(full, mine, group=g)  # in place
         else:  # gloo (CPU tests / ranks sharing one GPU)
             parts = list(full.chunk(world))
             dist.all_gather(parts, mine.clone(), group=g)
+
+    def _gather(self, slot: int) -> None:
+        rank, world, g, lo, hi = self.shard
+        esize = self.slots[slot].element_size()
+        self._gather_bytes(self.slots[slot].view(torch.uint8), (hi - lo) * esize, g)
 
     @property
     def block_nbytes(self) -> int:
