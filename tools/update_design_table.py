@@ -15,7 +15,8 @@ def fmt(x, nd=0):
 
 def main(tag="r1"):
     rows = []
-    for f in ["cfg1", "cfg2", "cfg2_fast", "cfg3", "cfg3_fast", "cfg4", "cfg4_fast", "cfg5"]:
+    for f in ["cfg1", "cfg2", "cfg2_fast", "cfg3", "cfg3_fast", "cfg4", "cfg4_fast", "cfg5",
+              "cfg5_fast"]:
         p = os.path.join(ROOT, "profiles", f"{tag}_bench_{f}.json")
         if not os.path.exists(p):
             continue
