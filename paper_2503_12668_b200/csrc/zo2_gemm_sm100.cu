@@ -858,7 +858,7 @@ struct AttnTcCfg {
   static constexpr int Q_OFF = 0;
   static constexpr int KV_OFF = Q_OFF + PL * PAN * QTILE;  // stage s: K at +2s*KV, V at +(2s+1)*KV
   static constexpr int BAR_OFF = KV_OFF + NS * 2 * KV;
-  static constexpr int SMEM = BAR_OFF + 256 + 4 * 128 * 4 + 1024;
+  static constexpr int SMEM = BAR_OFF + 256 + 6 * 128 * 4 + 1024;
   // TMEM columns (256 per CTA, two CTAs per SM): S buffers, O, P (bf16 pairs)
   static constexpr int SB = (HD + (SPLIT ? 64 : 32) + 2 * ATT_K <= 256) ? 2 : 1;
   static constexpr uint32_t T_O = SB * ATT_K;
@@ -895,7 +895,18 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
 // issues TMA and tcgen05.mma; the two sides meet only on mbarriers.  P goes
 // to TMEM (tcgen05.st) and is the A operand of P.V straight from there, so
 // a CTA needs no P staging in shared memory: two CTAs per SM.
+// p1 is a compile-time 0 in one-pass mode: `g >= p1` and friends fold away
+#pragma nv_diag_suppress 186
 constexpr int ATT_SOFT = 256;
+// 1: one pass over the key tiles with an online softmax (lazy O rescale);
+// 0: pass 1 takes the exact row max from Qhi.Khi, pass 2 computes P and P.V
+#ifndef ZO2_ATTN_ONEPASS
+#define ZO2_ATTN_ONEPASS 1
+#endif
+constexpr bool ATT_ONEPASS = ZO2_ATTN_ONEPASS != 0;
+// online softmax: the running max moves only when a row's tile max exceeds it
+// by more than 2^ATT_TAU (P values stay <= 2^ATT_TAU, O is rescaled rarely)
+constexpr float ATT_TAU = 8.0f;
 template <int HD, bool SPLIT>
 __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_constant__ AttnTcArgs a) {
   using C = AttnTcCfg<HD, SPLIT>;
@@ -909,13 +920,14 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
   uint64_t *bar_o = bar_p + 1;                         // P.V done (MMA commit)
   uint64_t *bar_kvfree = bar_o + 1;                    // [NS] ring stage read by its MMAs
   uint32_t *tmem_slot = (uint32_t *)(bar_kvfree + NS);
-  float *xch = (float *)(smem + C::BAR_OFF + 256);     // [2][128] row max, then [2][128] row sum
+  float *xch = (float *)(smem + C::BAR_OFF + 256);     // [2][2][128] row max, then [2][128] row sum
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // heavy (late) query tiles first
   const uint32_t qt = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int row0 = (int)(b * a.seq + qt * ATT_Q);
   const uint32_t n_kt = (qt + 1) * (ATT_Q / ATT_K);  // causal: key tiles up to the diagonal
-  const uint32_t n_all = 2 * n_kt;                   // pass 1 (K only) then pass 2 (K, V)
+  const uint32_t p1 = ATT_ONEPASS ? 0u : n_kt;        // pass-1 tiles (K only, row max)
+  const uint32_t n_all = p1 + n_kt;                  // then n_kt tiles of S, P and P.V
   const uint32_t d = a.dim;
 
   if (threadIdx.x == ATT_SOFT) {
@@ -950,8 +962,8 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
     if (lane == 0) {
       const uint32_t sq = smem_u32(smem + C::Q_OFF), skv = smem_u32(smem + C::KV_OFF);
       auto load_tile = [&](uint32_t g) {
-        const uint32_t j = g < n_kt ? g : g - n_kt;
-        const bool with_v = g >= n_kt, with_q = g == 0;
+        const uint32_t j = g < p1 ? g : g - p1;
+        const bool with_v = g >= p1, with_q = g == 0;
         const int st = (int)(g % NS);
         // pass 1 only needs the max of S, taken from Qhi Khi: K's lo plane stays home
         const int kpl = with_v ? C::PL : 1;
@@ -984,7 +996,7 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
           const uint32_t ko = (uint32_t)((ks / 4) * C::KTILE + (ks % 4) * 32);
           const uint64_t qa = sw128_desc(sq + qo), kd = sw128_desc(sk + ko);
           tc_mma(ts, qa, kd, id, ks != 0);
-          if (SPLIT && g >= n_kt) {  // pass 1 (row max only): Qhi Khi suffices
+          if (SPLIT && g >= p1) {  // pass 1 (row max only): Qhi Khi suffices
             tc_mma(ts, qa, sw128_desc(sk + C::PAN * C::KTILE + ko), id, 1u);
             tc_mma(ts, sw128_desc(sq + C::PAN * C::QTILE + qo), kd, id, 1u);
           }
@@ -993,7 +1005,7 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
       };
       // O += P(j) V(j): A = P [128 q x 64 keys] in TMEM, B = V [64 keys x hd] MN-major
       auto issue_pv = [&](uint32_t g) {
-        const uint32_t j = g - n_kt;
+        const uint32_t j = g - p1;
         constexpr uint32_t id = idesc_bf16_b(HD, true);
         constexpr uint32_t vlbo = (uint32_t)C::KTILE;  // next 64 hd columns: next panel
         const uint32_t sv = skv + (uint32_t)((2 * (int)(g % NS) + 1) * C::KV);
@@ -1014,7 +1026,7 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
       mbar_wait(&bar_kv[0], 0);
       tc_fence_after();
       issue_qk(0);
-      if (n_kt > 0) tc_commit(&bar_kvfree[0]);
+      if (p1 > 0) tc_commit(&bar_kvfree[0]);
       for (uint32_t g = 0; g < n_all; ++g) {
         // refill the ring stage of tile g - 1 (consumed by S(g - 1) / P.V(g - 1))
         if (g >= 1 && g - 1 + NS < n_all) {
@@ -1031,10 +1043,10 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
           if (gn >= (uint32_t)SB) mbar_wait(&bar_sfree[gn % SB], ((gn - SB) / SB) & 1u);
           tc_fence_after();
           issue_qk(gn);
-          if (gn < n_kt) tc_commit(&bar_kvfree[gn % NS]);  // pass 1: K read by S only
+          if (gn < p1) tc_commit(&bar_kvfree[gn % NS]);  // pass 1: K read by S only
         }
-        if (g >= n_kt) {  // P.V of this tile once the softmax stored P(j)
-          const uint32_t j = g - n_kt;
+        if (g >= p1) {  // P.V of this tile once the softmax stored P(j)
+          const uint32_t j = g - p1;
           mbar_wait(bar_p, j & 1u);
           tc_fence_after();
           issue_pv(g);
@@ -1048,10 +1060,10 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
     const int r = quad * 32 + lane;  // query row within the tile (TMEM lane)
     const int c0 = 32 * half;        // this warp's 32 columns of S
-    float mrow = -INFINITY, mscaled = 0.f, lsum = 0.f;
+    float mrow = -INFINITY, mscaled = ATT_ONEPASS ? -INFINITY : 0.f, lsum = 0.f;
     for (uint32_t g = 0; g < n_all; ++g) {
-      const bool pass2 = g >= n_kt;
-      const uint32_t j = pass2 ? g - n_kt : g;
+      const bool pass2 = ATT_ONEPASS || g >= p1;
+      const uint32_t j = pass2 ? g - p1 : g;
       const int lim = (int)(qt * ATT_Q) + r - (int)(j * ATT_K) - c0;  // visible: i <= lim
       mbar_wait(&bar_s[g % SB], (g / SB) & 1u);
       tc_fence_after();
@@ -1069,6 +1081,23 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
           mscaled = fmaxf(xch[r], xch[128 + r]) * a.scale_log2;
         }
         continue;
+      }
+      float alpha = 1.f;  // O and l rescale of this row (online softmax)
+      if (ATT_ONEPASS) {
+        float mt = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (i <= lim) mt = fmaxf(mt, __uint_as_float(v[i]));
+        // the two warps of a quadrant hold the halves of the same rows
+        float *slot = xch + (j & 1u) * 256;
+        slot[half * 128 + r] = mt;
+        asm volatile("bar.sync %0, 64;" ::"r"(2 + quad) : "memory");
+        mt = fmaxf(slot[r], slot[128 + r]) * a.scale_log2;
+        if (mt > mscaled + ATT_TAU) {
+          alpha = ex2f(mscaled - mt);
+          mscaled = mt;
+          lsum *= alpha;
+        }
       }
       float pv[32];
 #pragma unroll
@@ -1092,6 +1121,21 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
       if (j >= 1) {
         mbar_wait(bar_o, (j - 1) & 1u);
         tc_fence_after();
+        // O(j - 1) is final: rescale this warp's O columns if any row's max moved
+        if (ATT_ONEPASS && __any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll 1
+          for (int o0 = half * (HD / 2); o0 < (half + 1) * (HD / 2); o0 += 32) {
+            uint32_t w[32];
+            tmem_ld32(t_o + lane_base + (uint32_t)o0, w);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              uint32_t x[16];
+#pragma unroll
+              for (int e = 0; e < 16; ++e) x[e] = __float_as_uint(__uint_as_float(w[16 * q + e]) * alpha);
+              tmem_st16(t_o + lane_base + (uint32_t)(o0 + 16 * q), x);
+            }
+          }
+        }
       }
       tmem_st16(tmem + C::T_P + lane_base + (uint32_t)(c0 / 2), hi);
       if (SPLIT) tmem_st16(tmem + C::T_PLO + lane_base + (uint32_t)(c0 / 2), lo);
@@ -1100,11 +1144,11 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
       mbar_arrive(bar_p);
     }
     // ---------------------------------------------- epilogue: O / l -> bf16 planes
-    xch[256 + half * 128 + r] = lsum;
+    xch[512 + half * 128 + r] = lsum;
     mbar_wait(bar_o, (n_kt - 1) & 1u);  // last P.V (and so every P.V) done
     tc_fence_after();
     asm volatile("bar.sync 1, %0;" ::"n"(ATT_SOFT) : "memory");
-    const float inv = 1.0f / (xch[256 + r] + xch[384 + r]);
+    const float inv = 1.0f / (xch[512 + r] + xch[640 + r]);
     __nv_bfloat16 *oh = a.out_hi + (uint64_t)(row0 + r) * d + h * HD;
     __nv_bfloat16 *ol = SPLIT ? a.out_lo + (uint64_t)(row0 + r) * d + h * HD : nullptr;
 #pragma unroll 1
