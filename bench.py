@@ -327,7 +327,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                             capacity_bytes=cfg.get("cap", float("inf")), device=dev)
     eng = Zo2Engine(TransformerWorkload(params, cfg["arith"]),
                     ZOConfig(EPS, cfg["lr"], max(1, args.steps), SEED), rt, validate=True,
-                    operand_sets=args.operand_sets, rng=args.rng)
+                    operand_sets=args.operand_sets, rng=args.rng,
+                    pipeline_steps=not args.no_pipeline)
     sharded = False
     if world > 1:
         sharded = eng.enable_data_parallel(shard_transfers=shm is not None)
@@ -367,6 +368,13 @@ def run_ours(args, cfg, rank, world, local_rank):
         e0.record(comp)
         for k in range(args.steps):
             eng.step_async(j + k)
+        # the timed region ends when every lane is done (the last offload
+        # may trail the compute lane), not just the compute stream
+        for st in eng.lanes.streams.values():
+            if st is not comp:
+                ev = torch.cuda.Event()
+                ev.record(st)
+                comp.wait_event(ev)
         e1.record(comp)
         eng.drain()
         torch.cuda.synchronize()
@@ -374,7 +382,6 @@ def run_ours(args, cfg, rank, world, local_rank):
     barrier()
     j += args.steps
     dev_ms = e0.elapsed_time(e1)
-    # the last offload of the last step may end after the compute stream
     tls = [tl for _, tl in eng.timelines[n_tl0:]]
     ms = max_over_ranks(dev_ms)
     prof = eng.dev.fwd.prof
@@ -452,7 +459,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "compute": "3-pass bf16 split GEMM (f32-faithful)" if split else "bf16 GEMM",
                    "l2": "inputs larger than L2 (4.8+ GB of weights streamed per step)",
                    "rng": args.rng + (" (reference z stream, bit-exact)" if args.rng == "exact"
-                                      else " (Philox4x32 + binary32 erfinv, not the reference's z)")},
+                                      else " (Philox4x32 + binary32 erfinv, not the reference's z)"),
+                   "steps_pipelined": not args.no_pipeline},
         "roofline": {"bound": "tensor", "kernel": "zo2_gemm (tcgen05 cta_group::2, fused epilogues)",
                      "achieved": gemm_tflops, "peak": peak_bf16 / passes,
                      "unit": "TFLOP/s", "frac": (gemm_tflops * passes / peak_bf16
@@ -520,6 +528,8 @@ def main():
                          "transfers (default: one shared copy, sharded transfers)")
     ap.add_argument("--rng", default="exact", choices=["exact", "fast"],
                     help="z generator: the reference's stream (default) or the fast GPU one")
+    ap.add_argument("--no-pipeline", action="store_true",
+                    help="per-step device barrier instead of cross-step pipelining")
     ap.add_argument("--gemm-variant", type=int, default=0,
                     help="0 auto (CTA pair for large shapes), 1 single-CTA, 2 pair")
     args = ap.parse_args()

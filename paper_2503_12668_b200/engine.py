@@ -186,7 +186,13 @@ class _DeviceStep:
             self.fwd = DualForward(self.spec, batch_size, self.arith, self.device,
                                    self.operand_sets)
             T = self.fwd.T
-            self.h_tok = torch.empty(2, T, dtype=torch.int64, pin_memory=True)
+            # a ring of pinned staging buffers: step_async may enqueue several
+            # iterations before the first one's token copy has executed
+            self.h_tok_ring = [torch.empty(2, T, dtype=torch.int64, pin_memory=True)
+                               for _ in range(4)]
+            self.h_tok_ev = [None] * len(self.h_tok_ring)
+            self.h_tok_i = 0
+            self.h_tok = self.h_tok_ring[0]
         return self.fwd
 
     def stage_batch(self, batch, stream: torch.cuda.Stream) -> tuple[int, int]:
@@ -200,11 +206,17 @@ class _DeviceStep:
         if tokens.min() < 0 or tokens.max() >= self.spec.vocab:
             raise ValueError("token id out of range")
         fwd = self.ensure(tokens.shape[0])
+        i = self.h_tok_i = (self.h_tok_i + 1) % len(self.h_tok_ring)
+        if self.h_tok_ev[i] is not None:
+            self.h_tok_ev[i].synchronize()  # its previous copy has been read
+        self.h_tok = self.h_tok_ring[i]
         self.h_tok[0].numpy()[:] = tokens.reshape(-1)
         self.h_tok[1].numpy()[:] = targets.reshape(-1)
         with torch.cuda.stream(stream):
             fwd.ids.copy_(self.h_tok[0], non_blocking=True)
             fwd.targets.copy_(self.h_tok[1], non_blocking=True)
+            ev = self.h_tok_ev[i] = torch.cuda.Event()
+            ev.record(stream)
         return tokens.shape[0], tokens.shape[1]
 
     def read_out(self, stream: torch.cuda.Stream) -> None:
@@ -219,7 +231,7 @@ class Zo2Engine:
     def __init__(self, workload: TransformerWorkload, cfg: ZOConfig, runtime: OffloadRuntime,
                  *, overlap: bool = True, backend: str = "cuda", update_mode: str = "deferred",
                  cost=None, trace=None, validate: bool = True, prepare_lane: bool = True,
-                 operand_sets: int = 1, rng: str = "exact"):
+                 operand_sets: int = 1, rng: str = "exact", pipeline_steps: bool = True):
         if update_mode not in ("deferred", "naive"):
             raise ValueError(f"unknown update_mode {update_mode!r}")
         if rng not in RNG_MODES:
@@ -252,6 +264,10 @@ class Zo2Engine:
         _lib.call("zo2_set_k2_ctas_per_sm", conc if self.operand_sets >= 2 else 0)
         self._pool_booked = False
         self._async: list = []
+        # cross-step pipelining: the previous iteration
+        # whose tail the next one overlaps instead of a full step barrier
+        self.pipeline_steps = pipeline_steps
+        self._prev_enq = None
         self._hist = torch.zeros(64, 4, dtype=torch.float64, device=runtime.device)
         # data parallel: loss sums are all-reduced before g is formed (K10)
         self.dist_group = None
@@ -504,13 +520,41 @@ class Zo2Engine:
         if naive:
             for m in self._order:
                 fns[ckey(m, 2)] = lambda st, m=m: self._naive_update(m, step_index, st)
-        enq = enqueue_dag(dag, self.lanes, fns)
+        carry = None if naive or not self.prepare_lane else self._carry()
+        prev = self._prev_enq
+        enq = enqueue_dag(dag, self.lanes, fns, carry=carry,
+                          base=None if prev is None else prev.origin_event)
         close_step(self.lanes)
+        self._prev_enq = enq if (self.pipeline_steps and not naive and self.prepare_lane) else None
         expected = 0 if naive else len(self._order)
         if len(self.mgr.rsb) != expected:
             raise StateCorruptionError(f"rsb holds {len(self.mgr.rsb)} entries, "
                                        f"expected {expected}")
         return enq, dag, rt.take_records()
+
+    def _carry(self):
+        """Cross-step edges replacing the per-step barrier (None: barrier).
+
+        Next to stream order on each lane, iteration j+1 depends on iteration
+        j only through
+          * the arena ring: U(i, j+1), i < K, waits for the offload of the last
+            block of iteration j that used slot i % K;
+          * g_j: the first prepare task (K2 applies the deferred update with
+            g_j, and reuses operand sets C(., j) read) waits for C(head, j).
+        The compute lane (embed updates in place with g_j, head forms g) and
+        the offload lane stay in stream order."""
+        prev = self._prev_enq
+        if prev is None:
+            return None
+        rt, blocks = self.runtime, self._blocks
+        carry: dict[str, list] = {}
+        k = rt.k_slots
+        for i in range(min(k, len(blocks))):
+            last = max(m for m in range(len(blocks)) if rt.slot_for(m) == rt.slot_for(i))
+            carry[ukey(blocks[i])] = [prev.end_event(okey(blocks[last]))]
+        first_p = pkey(blocks[0]) if blocks else pkey(self._order[-1])
+        carry[first_p] = [prev.end_event(ckey(self._order[-1]))]
+        return carry
 
     def force_pending(self, g: float) -> None:
         """Parity hook: replace the pending projected gradient with an
@@ -553,6 +597,7 @@ class Zo2Engine:
             comp.synchronize()
         self.pending.clear()
         self.mgr.rsb.clear()
+        self._prev_enq = None
         return rt.export_params()
 
     def train(self, dataset, steps: int | None = None) -> list[float]:

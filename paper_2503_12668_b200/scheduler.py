@@ -334,8 +334,12 @@ class EnqueuedStep:
     """Events of one enqueued DAG; timeline() is valid after synchronisation."""
 
     def __init__(self, dag: TaskDag, origin: torch.cuda.Event,
-                 marks: dict[str, tuple[Lane, str, torch.cuda.Event, torch.cuda.Event]]):
-        self.dag, self.origin, self.marks = dag, origin, marks
+                 marks: dict[str, tuple[Lane, str, torch.cuda.Event, torch.cuda.Event]],
+                 rebase: bool = False, origin_event: torch.cuda.Event | None = None):
+        # origin: the timing base; origin_event: this iteration's own start
+        # mark on the compute lane (the next pipelined iteration's base)
+        self.dag, self.origin, self.marks, self.rebase = dag, origin, marks, rebase
+        self.origin_event = origin if origin_event is None else origin_event
 
     def end_event(self, key: str) -> torch.cuda.Event:
         return self.marks[key][3]
@@ -346,24 +350,40 @@ class EnqueuedStep:
             t0 = self.origin.elapsed_time(s) * 1e-3
             t1 = self.origin.elapsed_time(e) * 1e-3
             evs.append(StreamEvent(lane, key, module, t0, t1))
+        if self.rebase and evs:
+            t_min = min(e.t_start for e in evs)
+            evs = [StreamEvent(e.lane, e.key, e.module, e.t_start - t_min, e.t_end - t_min)
+                   for e in evs]
         evs.sort(key=lambda x: (x.t_start, x.key))
         return Timeline(evs)
 
 
 def enqueue_dag(dag: TaskDag, lanes: CudaLanes, task_fns: Mapping[str, Callable],
-                after: torch.cuda.Event | None = None) -> EnqueuedStep:
+                after: torch.cuda.Event | None = None,
+                carry: Mapping[str, list] | None = None,
+                base: torch.cuda.Event | None = None) -> EnqueuedStep:
     """Enqueue every task of `dag` on its lane's stream; returns immediately.
 
     task_fns[key](stream) enqueues the task's work on `stream`.  `after`
-    (optional) is an event every lane waits on first (previous step's tail)."""
-    lanes.barrier_in()
+    (optional) is an event every lane waits on first (previous step's tail).
+
+    Without `carry` the iteration starts behind a device-side barrier on the
+    previous iteration's tail on every lane (the reference's per-step barrier,
+    zo2_engine.py:295).  With `carry` (cross-step pipelining)
+    there is no barrier: carry[key] lists the previous iteration's events
+    task `key` must wait for, on top of stream order.  `base` is then an event
+    known to precede every task of this iteration (the previous iteration's
+    origin); timelines are measured from it and shifted to start at 0."""
+    if carry is None:
+        lanes.barrier_in()
     if after is not None:
         for lane in Lane:
             lanes[lane].wait_event(after)
     origin = torch.cuda.Event(enable_timing=True)
     origin.record(lanes[Lane.COMPUTE])
-    for lane in (Lane.UPLOAD, Lane.OFFLOAD, Lane.PREPARE):
-        lanes[lane].wait_event(origin)
+    if carry is None:
+        for lane in (Lane.UPLOAD, Lane.OFFLOAD, Lane.PREPARE):
+            lanes[lane].wait_event(origin)
     marks: dict = {}
     for task in topological_order(dag):
         stream = lanes[task.lane]
@@ -371,6 +391,9 @@ def enqueue_dag(dag: TaskDag, lanes: CudaLanes, task_fns: Mapping[str, Callable]
             plane = dag.by_key[p].lane
             if plane is not task.lane:
                 stream.wait_event(marks[p][3])
+        if carry is not None:
+            for ev in carry.get(task.key, ()):
+                stream.wait_event(ev)
         s = torch.cuda.Event(enable_timing=True)
         e = torch.cuda.Event(enable_timing=True)
         s.record(stream)
@@ -379,6 +402,8 @@ def enqueue_dag(dag: TaskDag, lanes: CudaLanes, task_fns: Mapping[str, Callable]
             fn(stream)
         e.record(stream)
         marks[task.key] = (task.lane, task.module, s, e)
+    if carry is not None and base is not None:
+        return EnqueuedStep(dag, base, marks, rebase=True, origin_event=origin)
     return EnqueuedStep(dag, origin, marks)
 
 
