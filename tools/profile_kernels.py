@@ -49,7 +49,37 @@ def k2(arith="f32"):
     torch.cuda.synchronize()
 
 
+def head(arith="f32"):
+    """Head GEMM with the fused cross-entropy epilogue (K7) + CE reduce."""
+    spec = ModelSpec(1, 2048, 32, 50272, 512)
+    fwd = DualForward(spec, 16, arith, "cuda", 1)
+    for t in fwd.h:
+        t.normal_()
+    for o in fwd.head_op:
+        o.hi.normal_(0, 0.02)
+        if o.lo is not None:
+            o.lo.normal_(0, 1e-5)
+    fwd.targets.random_(0, spec.vocab)
+    s = torch.cuda.current_stream().cuda_stream
+    for _ in range(2):
+        fwd.head_forward(s)
+    torch.cuda.synchronize()
+
+
+def embed(arith="f32"):
+    """Embedding gather with the on-the-fly update + perturbation (K8)."""
+    spec = ModelSpec(1, 2048, 32, 50272, 512)
+    fwd = DualForward(spec, 16, arith, "cuda", 1)
+    table = torch.randn((spec.vocab + spec.seq_len) * spec.dim, device="cuda") * 0.02
+    fwd.ids.random_(0, spec.vocab)
+    d_g = torch.tensor([1.5], dtype=torch.float64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    for j in range(2):
+        fwd.embed_forward(table, 0, True, d_g, 1e-7, 11 + j, 1e-3, 12 + j, spec.seq_len, s)
+    torch.cuda.synchronize()
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "fwd"
     arith = sys.argv[2] if len(sys.argv) > 2 else "f32"
-    (k2 if what == "k2" else main)(arith)
+    {"k2": k2, "head": head, "embed": embed}.get(what, main)(arith)

@@ -15,4 +15,10 @@ ZO2_RNG=fast ncu --set full --import-source on -k regex:k_update_perturb -c 1 \
     -o gpurun_out/${R}_k2_fast python tools/profile_kernels.py k2 f32 > /dev/null 2>&1
 ncu --set full --import-source on -k regex:k_attn -c 1 \
     -o gpurun_out/${R}_attention python tools/profile_kernels.py fwd f32 > /dev/null 2>&1
+ncu --set full --import-source on -k regex:k_layernorm -c 1 \
+    -o gpurun_out/${R}_layernorm python tools/profile_kernels.py fwd f32 > /dev/null 2>&1
+ncu --set full --import-source on -k regex:k_gemm --launch-skip 1 --launch-count 1 \
+    -o gpurun_out/${R}_gemm_head_ce python tools/profile_kernels.py head f32 > /dev/null 2>&1
+ncu --set full --import-source on -k regex:k_embed -c 1 \
+    -o gpurun_out/${R}_embed python tools/profile_kernels.py embed f32 > /dev/null 2>&1
 ls -la gpurun_out | grep $R
