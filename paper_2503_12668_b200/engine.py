@@ -30,7 +30,8 @@ from .model import (EMBED_ID, HEAD_ID, DualForward, ModelSpec, module_order, mod
 from .numerics import BATCH_STREAM, PERTURB_STREAM, RngState, derive_step_seed, raw_uint64
 from .runtime import ModelParams, OffloadRuntime
 from .scheduler import (CudaLanes, Lane, build_iteration_dag, build_prepare_dag, ckey,
-                        close_step, enqueue_dag, okey, pkey, ukey, validate_timeline)
+                        close_step, cross_step_edges, enqueue_dag, okey, pkey, ukey,
+                        validate_timeline)
 
 
 # z generator per engine (zo2b200.h zo2_set_rng_mode): "exact" is the
@@ -533,28 +534,13 @@ class Zo2Engine:
         return enq, dag, rt.take_records()
 
     def _carry(self):
-        """Cross-step edges replacing the per-step barrier (None: barrier).
-
-        Next to stream order on each lane, iteration j+1 depends on iteration
-        j only through
-          * the arena ring: U(i, j+1), i < K, waits for the offload of the last
-            block of iteration j that used slot i % K;
-          * g_j: the first prepare task (K2 applies the deferred update with
-            g_j, and reuses operand sets C(., j) read) waits for C(head, j).
-        The compute lane (embed updates in place with g_j, head forms g) and
-        the offload lane stay in stream order."""
+        """Cross-step edges replacing the per-step barrier (None: barrier);
+        see scheduler.cross_step_edges."""
         prev = self._prev_enq
         if prev is None:
             return None
-        rt, blocks = self.runtime, self._blocks
-        carry: dict[str, list] = {}
-        k = rt.k_slots
-        for i in range(min(k, len(blocks))):
-            last = max(m for m in range(len(blocks)) if rt.slot_for(m) == rt.slot_for(i))
-            carry[ukey(blocks[i])] = [prev.end_event(okey(blocks[last]))]
-        first_p = pkey(blocks[0]) if blocks else pkey(self._order[-1])
-        carry[first_p] = [prev.end_event(ckey(self._order[-1]))]
-        return carry
+        edges = cross_step_edges(self._blocks, self._order[-1], self.runtime.k_slots)
+        return {k: [prev.end_event(p) for p in ps] for k, ps in edges.items()}
 
     def force_pending(self, g: float) -> None:
         """Parity hook: replace the pending projected gradient with an

@@ -358,6 +358,29 @@ class EnqueuedStep:
         return Timeline(evs)
 
 
+def cross_step_edges(block_ids: list[str], head_id: str, k_slots: int) -> dict[str, list[str]]:
+    """Edges from iteration j to iteration j+1 of the prepare DAG that replace
+    the per-step barrier (cross-step pipelining):
+    {task of j+1: [tasks of j it waits for]}.  Next to FIFO order on each lane:
+
+      * the arena ring: U(i, j+1), i < K, waits for the offload of the last
+        block of iteration j that used slot i % K (slot_for(i) = i % K,
+        runtime.py:202-304); blocks i >= K follow through U(i-K.. ) edges;
+      * g_j: the first prepare task waits for C(head, j) -- K2 applies the
+        deferred update with g_j and rewrites operand sets C(., j) read.
+
+    The compute lane (the embedding updates in place with g_j, the head forms
+    g) and the offload lane need nothing beyond FIFO order."""
+    n = len(block_ids)
+    out: dict[str, list[str]] = {}
+    for i in range(min(k_slots, n)):
+        last = max(m for m in range(n) if m % k_slots == i % k_slots)
+        out[ukey(block_ids[i])] = [okey(block_ids[last])]
+    first_p = pkey(block_ids[0]) if n else pkey(head_id)
+    out[first_p] = [ckey(head_id)]
+    return out
+
+
 def enqueue_dag(dag: TaskDag, lanes: CudaLanes, task_fns: Mapping[str, Callable],
                 after: torch.cuda.Event | None = None,
                 carry: Mapping[str, list] | None = None,

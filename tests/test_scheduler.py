@@ -94,3 +94,57 @@ def test_chrome_trace_rows():
     rows = _simulate(d, lambda t: 1e-3).chrome_trace_rows(step=4)
     assert {r["tid"] for r in rows} == {0, 1, 2, 3}
     assert all(r["ph"] == "X" and r["args"]["step"] == 4 for r in rows)
+
+
+@pytest.mark.parametrize("n,k,sets", [(6, 3, 1), (7, 3, 1), (9, 4, 2), (2, 3, 1), (1, 3, 1),
+                                      (5, 2, 1)])
+def test_cross_step_edges_keep_every_hazard(n, k, sets):
+    """Two pipelined iterations (per-lane FIFO + each DAG + cross_step_edges,
+    no barrier) scheduled with random durations never violate a cross-step
+    hazard: a slot is re-uploaded only after its previous tenant's offload, a
+    block's host master is read only after it was written back, K2 of j+1 runs
+    after g_j exists and after C(., j) released the operand sets."""
+    import random
+    from paper_2503_12668_b200.scheduler import HEAD_ID as head
+    from paper_2503_12668_b200.scheduler import cross_step_edges
+    blocks = [f"block.{i}" for i in range(n)]
+    d = build_prepare_dag(blocks, k_slots=k, operand_sets=sets)
+    cross = cross_step_edges(blocks, head, k)
+
+    def tag(key, j):
+        return f"{key}@{j}"
+    tasks, edges = [], []
+    for j in (0, 1):
+        tasks += [TaskSpec(tag(t.key, j), t.lane, t.module, t.kind, t.bytes, t.phase)
+                  for t in d.tasks]
+        edges += [(tag(a, j), tag(b, j)) for a, b in d.edges]
+    edges += [(tag(p, 0), tag(c, 1)) for c, ps in cross.items() for p in ps]
+    # lane FIFO across the iteration boundary: every task of j on a lane
+    # precedes every task of j+1 on it (stream order)
+    for lane in Lane:
+        t0 = [tag(t.key, 0) for t in topological_order(d) if t.lane is lane]
+        t1 = [tag(t.key, 1) for t in topological_order(d) if t.lane is lane]
+        if t0 and t1:
+            edges.append((t0[-1], t1[0]))
+    two = TaskDag(tasks, edges)
+    rnd = random.Random(n * 100 + k * 10 + sets)
+    for _ in range(20):
+        dur = {t.key: rnd.uniform(0.1, 3.0) for t in two.tasks}
+        ev = _simulate(two, lambda t: dur[t.key]).by_key()
+        for i, b in enumerate(blocks):
+            # same slot: every block of j in slot i % k is offloaded before U(i, j+1)
+            for m, b2 in enumerate(blocks):
+                if m % k == i % k:
+                    assert ev[tag(okey(b2), 0)].t_end <= ev[tag(ukey(b), 1)].t_start
+            # host master of block b written back (O(b, j)) before read (U(b, j+1))
+            assert ev[tag(okey(b), 0)].t_end <= ev[tag(ukey(b), 1)].t_start
+            # K2(b, j+1) needs g_j and free operand sets
+            assert ev[tag(ckey(head), 0)].t_end <= ev[tag(pkey(b), 1)].t_start
+            for b2 in blocks:
+                assert ev[tag(ckey(b2), 0)].t_end <= ev[tag(pkey(b), 1)].t_start
+        assert ev[tag(ckey(head), 0)].t_end <= ev[tag(pkey(head), 1)].t_start
+        # and pipelining does overlap: U(0, j+1) need not wait for C(head, j)
+    if n > k:
+        dur = {t.key: (5.0 if t.lane is Lane.COMPUTE else 1.0) for t in two.tasks}
+        ev = _simulate(two, lambda t: dur[t.key]).by_key()
+        assert ev[tag(ukey(blocks[0]), 1)].t_start < ev[tag(ckey(head), 0)].t_end
