@@ -77,6 +77,30 @@ def peaks():
 # ----------------------------------------------------------------------------
 # clocks sampler (nvidia-smi during the timed region)
 # ----------------------------------------------------------------------------
+# K2 is bound by instruction issue, not HBM: warp instructions per draw from
+# the ncu capture of one OPT-1.3B block (smsp__inst_executed.sum / 2 n draws,
+# profiles/r1_ncu_full_k2_{exact,fast}.txt, n = 50 358 272)
+K2_WARP_INST_PER_DRAW = {"exact": 753229633 / (2 * 50358272),
+                         "fast": 440114924 / (2 * 50358272)}
+
+
+def k2_issue_roofline(draws, ms, rng, clocks, dev):
+    """K2's roofline: one warp instruction per SM sub-partition per clock at
+    the SM clock measured during the run; achieved = draws per second."""
+    if not ms:
+        return None
+    import torch
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    ipd = K2_WARP_INST_PER_DRAW[rng]
+    limit = 4 * sms * mhz * 1e6 / ipd / 1e9
+    got = draws / (ms * 1e-3) / 1e9
+    return {"bound": "issue", "achieved": got, "peak": limit, "unit": "Gdraws/s",
+            "frac": got / limit, "warp_inst_per_draw": ipd, "sm_mhz": mhz,
+            "note": "peak = 4 SMSPs x SMs x SM clock / warp instructions per draw "
+                    "(ncu, profiles/r1_ncu_full_k2_*.txt); HBM is ~6% utilised"}
+
+
 class Clocks:
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -475,7 +499,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "tensor_passes": passes,
                      "gemm_ms_per_step": gemm_ms / args.steps,
                      "k2_ms_per_step": k2_ms / args.steps,
-                     "k2_gdraws_per_s": (k2_draws / (k2_ms * 1e-3) / 1e9) if k2_ms else None},
+                     "k2_gdraws_per_s": (k2_draws / (k2_ms * 1e-3) / 1e9) if k2_ms else None,
+                     "k2": k2_issue_roofline(k2_draws, k2_ms, args.rng, clk.summary(), dev)},
         "step_roofline": {"bound": "pcie" if (t_link or 0) >= t_tensor else "tensor",
                           "link_probe_gbs": {"h2d": probe_up, "d2h": probe_dn,
                                              "note": "1 GiB pinned copies, both directions "
