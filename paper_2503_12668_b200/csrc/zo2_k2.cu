@@ -45,6 +45,9 @@ constexpr int MAX_SEGS = 16;
 #ifndef ZO2_K2_CENTRAL_X2
 #define ZO2_K2_CENTRAL_X2 1
 #endif
+#ifndef ZO2_K2_TAIL_X2
+#define ZO2_K2_TAIL_X2 1
+#endif
 #ifndef ZO2_K2_MINB
 #define ZO2_K2_MINB 4  // 64 registers (a few spills in cold paths): 4 CTAs (32 warps) per SM
 #endif
@@ -347,6 +350,17 @@ __device__ __forceinline__ void k2_tiles(void *arena, const K2Table &T, const K2
       const unsigned cnts = sm.counts[buf];
       const int nt = (int)(cnts & 0xffffu), nc = (int)(cnts >> 16), ntot = nt + nc;
       int i0 = warp * 32;
+#if ZO2_K2_TAIL_X2
+      // two pure-tail chunks per trip: two independent FP64 chains per lane
+      for (; i0 + NT + 32 <= nt; i0 += 2 * NT) {
+        const unsigned ea = sm.q[i0 + lane], eb = sm.q[i0 + NT + lane];
+        const int za = (int)(ea & 0x7FFFu), zb = (int)(eb & 0x7FFFu);
+        const double ra = zx_ndtri_tail(sm.z[za], (ea >> 15) != 0, sm.logtab, sm.tcoef);
+        const double rb = zx_ndtri_tail(sm.z[zb], (eb >> 15) != 0, sm.logtab, sm.tcoef);
+        sm.z[za] = ra;
+        sm.z[zb] = rb;
+      }
+#endif
       // chunks holding tail entries (the last one may also hold centrals)
       for (; i0 < nt; i0 += NT) {
         const int i = i0 + lane;
