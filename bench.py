@@ -484,7 +484,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "l2": "inputs larger than L2 (4.8+ GB of weights streamed per step)",
                    "rng": args.rng + (" (reference z stream, bit-exact)" if args.rng == "exact"
                                       else " (Philox4x32 + binary32 erfinv, not the reference's z)"),
-                   "steps_pipelined": not args.no_pipeline},
+                   "steps_pipelined": not args.no_pipeline,
+                   "operand_sets": eng.operand_sets},
         "roofline": {"bound": "tensor", "kernel": "zo2_gemm (tcgen05 cta_group::2, fused epilogues)",
                      "achieved": gemm_tflops, "peak": peak_bf16 / passes,
                      "unit": "TFLOP/s", "frac": (gemm_tflops * passes / peak_bf16
@@ -546,8 +547,9 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--operand-sets", type=int, default=1,
-                    help="1: K2 of block i+1 after the forward of block i; 2: concurrent")
+    ap.add_argument("--operand-sets", type=int, default=None,
+                    help="1: K2 of block i+1 after the forward of block i; 2: beside it "
+                         "(default: 2 when the device capacity admits two sets)")
     ap.add_argument("--replicated-masters", action="store_true",
                     help="data parallel: private host masters per rank and full-block "
                          "transfers (default: one shared copy, sharded transfers)")

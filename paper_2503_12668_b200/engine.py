@@ -232,7 +232,8 @@ class Zo2Engine:
     def __init__(self, workload: TransformerWorkload, cfg: ZOConfig, runtime: OffloadRuntime,
                  *, overlap: bool = True, backend: str = "cuda", update_mode: str = "deferred",
                  cost=None, trace=None, validate: bool = True, prepare_lane: bool = True,
-                 operand_sets: int = 1, rng: str = "exact", pipeline_steps: bool = True):
+                 operand_sets: int | None = None, rng: str = "exact",
+                 pipeline_steps: bool = True):
         if update_mode not in ("deferred", "naive"):
             raise ValueError(f"unknown update_mode {update_mode!r}")
         if rng not in RNG_MODES:
@@ -255,14 +256,16 @@ class Zo2Engine:
         self._order = [h.module for h in workload.modules()]
         self._blocks = [m for m in self._order if self._handles[m].transferable]
         self.prepare_lane = prepare_lane
-        self.operand_sets = operand_sets if prepare_lane and update_mode == "deferred" else 1
+        # operand sets: 2 lets K2 of block i+1 run beside the forward of block i
+        # (None = 2 unless the device capacity only admits one set)
+        self._sets_auto = operand_sets is None and prepare_lane and update_mode == "deferred"
+        if prepare_lane and update_mode == "deferred":
+            self.operand_sets = 2 if operand_sets is None else int(operand_sets)
+        else:
+            self.operand_sets = 1
         self.lanes = CudaLanes(runtime.device)
         self.dev = _DeviceStep(workload.spec, workload.arith, runtime.device, self.operand_sets)
-        # concurrent prepare lane: one K2 CTA per SM beside the persistent GEMM;
-        # otherwise K2 fills the GPU (grid from occupancy)
-        import os
-        conc = int(os.environ.get("ZO2_K2_CONCURRENT_CTAS", "1"))
-        _lib.call("zo2_set_k2_ctas_per_sm", conc if self.operand_sets >= 2 else 0)
+        self._set_k2_grid()
         self._pool_booked = False
         self._async: list = []
         # cross-step pipelining: the previous iteration
@@ -273,6 +276,31 @@ class Zo2Engine:
         # data parallel: loss sums are all-reduced before g is formed (K10)
         self.dist_group = None
         self.world = 1
+
+    def _set_k2_grid(self) -> None:
+        # K2 grid from occupancy (0) also beside the forward: measured faster
+        # than capping it at 1-2 CTAs per SM (tools/ab_sets.sh)
+        import os
+        conc = int(os.environ.get("ZO2_K2_CONCURRENT_CTAS", "0"))
+        _lib.call("zo2_set_k2_ctas_per_sm", conc if self.operand_sets >= 2 else 0)
+
+    def _choose_operand_sets(self, batch_size: int) -> None:
+        """Auto mode: drop to one operand set when two would not fit the
+        device capacity (DevicePool, runtime.py:94-142)."""
+        if not self._sets_auto:
+            return
+        fwd = self.dev.fwd
+        if fwd is not None and fwd.B == batch_size:
+            return
+        pool = self.runtime.pool
+        need = DualForward.estimate_nbytes(self.workload.spec, batch_size,
+                                           self.workload.arith, 2)
+        sets = 2 if pool.used + need <= pool.capacity else 1
+        if sets != self.operand_sets:
+            self.operand_sets = sets
+            self.dev.operand_sets = sets
+            self.dev.fwd = None
+            self._set_k2_grid()
 
     def enable_data_parallel(self, group=None, shard_transfers: bool = False) -> bool:
         """Shard the batch over torch.distributed ranks: every rank perturbs with
@@ -488,6 +516,7 @@ class Zo2Engine:
         self.mgr.begin_iteration(derive_step_seed(cfg.seed, step_index))
         comp = self.lanes[Lane.COMPUTE]
         if batch is not None:
+            self._choose_operand_sets(int(np.asarray(batch[0]).shape[0]))
             _, seq = self.dev.stage_batch(batch, comp)
         elif self.dev.fwd is None:
             raise ValueError("step_async(batch=None) needs a batch staged by an earlier step")

@@ -246,6 +246,18 @@ class DualForward:
         self._seg_cache: dict = {}
 
     # ---------------------------------------------------------------- sizes
+    @staticmethod
+    def estimate_nbytes(spec: ModelSpec, batch_size: int, arith: str,
+                        operand_sets: int = 1) -> int:
+        """Bytes the constructor allocates (same accounting as nbytes())."""
+        d, V, T = spec.dim, spec.vocab, int(batch_size) * spec.seq_len
+        ob = 4 if arith == "f32" else 2  # operand bytes per element (split: hi + lo)
+        act = 2 * T * d * 4 + 2 * ob * T * (d + 3 * d + d + 4 * d)
+        segs = segments(block_layout(spec))
+        per_set = sum(2 * sg.size * (4 if len(sg.shape) == 1 else ob) for sg in segs)
+        act += 2 * T * ((V + 127) // 128) * 3 * 4  # CE partials (N tile >= 128)
+        return act + operand_sets * per_set + 2 * V * d * ob + 2 * T * 8
+
     def nbytes(self) -> dict[str, int]:
         act = sum(t.numel() * t.element_size() for t in self.h)
         act += sum(o.nbytes for o in self.xop + self.ctx + self.mid + self.qkv)

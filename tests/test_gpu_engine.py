@@ -168,3 +168,29 @@ def test_cross_step_pipelining_bit_identical(cuda, golden, k):
     # every iteration's own DAG still validated on device timestamps
     assert len(eng.timelines) == G["steps"]
     assert all(min(e.t_start for e in tl.events) >= 0.0 for _, tl in eng.timelines)
+
+
+def test_operand_sets_auto_and_estimate(cuda, golden):
+    """Two operand sets by default; the size estimate used for the choice
+    equals what DualForward allocates; a capacity that only admits one set
+    makes the engine fall back to one (and still run bit-identically)."""
+    from paper_2503_12668_b200.model import DualForward, ModelSpec
+    for spec, B, arith, sets in [(ModelSpec(2, 64, 4, 96, 32), 3, "f32", 2),
+                                 (ModelSpec(1, 128, 2, 50272, 64), 2, "bf16", 1)]:
+        f = DualForward(spec, B, arith, "cuda", sets)
+        assert DualForward.estimate_nbytes(spec, B, arith, sets) >= sum(f.nbytes().values())
+        assert DualForward.estimate_nbytes(spec, B, arith, sets) <= 1.01 * sum(f.nbytes().values())
+    G, eng, batches = _setup(golden)
+    assert eng.operand_sets == 2
+    for j, b in enumerate(batches[:3]):
+        eng.step(b, j)
+    ref = list(eng.gs)
+    G, eng1, batches = _setup(golden)
+    spec = eng1.workload.spec
+    one = DualForward.estimate_nbytes(spec, G["batch_size"], "f32", 1)
+    two = DualForward.estimate_nbytes(spec, G["batch_size"], "f32", 2)
+    eng1.runtime.pool.capacity = eng1.runtime.pool.used + (one + two) // 2
+    for j, b in enumerate(batches[:3]):
+        eng1.step(b, j)
+    assert eng1.operand_sets == 1
+    assert eng1.gs == ref

@@ -22,8 +22,7 @@ def main(name="cfg2", steps=3):
     params = init_params(spec, RngState(1), device=dev, codec=cfg["codec"])
     rt = OffloadRuntime(params, k_slots=cfg["slots"], codec=cfg["codec"],
                         capacity_bytes=cfg.get("cap", float("inf")), device=dev)
-    eng = Zo2Engine(TransformerWorkload(params, cfg["arith"]), ZOConfig(1e-3, cfg["lr"], steps, 1), rt,
-                    operand_sets=1)
+    eng = Zo2Engine(TransformerWorkload(params, cfg["arith"]), ZOConfig(1e-3, cfg["lr"], steps, 1), rt)
     ds = gen_synthetic(V, S, 64, RngState(1), "affine", cfg["B"])
     eng.step(ds.batch(shard_indices(1, 0, 64, cfg["B"], 0, 1)), 0)
     for j in range(1, steps + 1):
