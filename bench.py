@@ -498,6 +498,9 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "algorithmic": "2*M*N*K per GEMM, summed over the step's GEMM launches "
                                     "(CUDA events on the compute stream)",
                      "tensor_passes": passes,
+                     "co_running": ("operand_sets=2: K2 of block i+1 shares the SMs with the "
+                                    "forward of block i, so GEMM and K2 launch durations "
+                                    "include that sharing" if eng.operand_sets >= 2 else None),
                      "gemm_ms_per_step": gemm_ms / args.steps,
                      "k2_ms_per_step": k2_ms / args.steps,
                      "k2_gdraws_per_s": (k2_draws / (k2_ms * 1e-3) / 1e9) if k2_ms else None,

@@ -253,7 +253,9 @@ template <int BN, bool SPLIT, int EPI>
 __global__ void __launch_bounds__(NUM_THREADS, 1) k_gemm(const __grid_constant__ GemmArgs args) {
   using C = Cfg<BN, SPLIT>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // aligned by offset, not through an integer cast: the pointer stays in the
+  // shared window, so plain loads/stores through it compile to LDS/STS
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t *full = (uint64_t *)(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t *empty = full + C::STAGES;
   uint64_t *tfull = empty + C::STAGES;
@@ -501,7 +503,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   using C = Cfg2<SPLIT>;
   constexpr int BN = C::BN;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // aligned by offset, not through an integer cast: the pointer stays in the
+  // shared window, so plain loads/stores through it compile to LDS/STS
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t *full = (uint64_t *)(smem + C::STAGES * C::STAGE_BYTES);
   uint64_t *empty = full + C::STAGES;
   uint64_t *tfull = empty + C::STAGES;
@@ -912,7 +916,9 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
   using C = AttnTcCfg<HD, SPLIT>;
   constexpr int NS = C::NS, SB = C::SB;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // aligned by offset, not through an integer cast: the pointer stays in the
+  // shared window, so plain loads/stores through it compile to LDS/STS
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t *bar_kv = (uint64_t *)(smem + C::BAR_OFF);  // [NS] tile loaded (TMA)
   uint64_t *bar_s = bar_kv + NS;                       // [SB] S written (MMA commit)
   uint64_t *bar_sfree = bar_s + 2;                     // [SB] S read (256 arrivals)

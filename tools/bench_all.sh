@@ -9,6 +9,7 @@ timeout 1200 python bench.py --config cfg4 --steps 2 --warmup 3 --no-cpu-baselin
 timeout 1200 python bench.py --config cfg4 --steps 2 --warmup 3 --no-cpu-baseline --rng fast > gpurun_out/${R}_bench_cfg4_fast.json 2> gpurun_out/${R}_bench_cfg4_fast.err
 timeout 600 python bench.py --config cfg1 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/${R}_bench_cfg1.json 2> gpurun_out/${R}_bench_cfg1.err
 timeout 1500 python bench.py --config cfg5 --steps 2 --warmup 2 --no-cpu-baseline > gpurun_out/${R}_bench_cfg5.json 2> gpurun_out/${R}_bench_cfg5.err
+timeout 1500 python bench.py --config cfg5 --steps 2 --warmup 2 --no-cpu-baseline --rng fast > gpurun_out/${R}_bench_cfg5_fast.json 2> gpurun_out/${R}_bench_cfg5_fast.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${R}_bench_reference.json 2> gpurun_out/${R}_bench_reference.err
 for f in gpurun_out/${R}_bench_*.json; do python - "$f" <<'PY'
 import json, sys
