@@ -863,13 +863,13 @@ struct AttnTcCfg {
   static constexpr int KV_OFF = Q_OFF + PL * PAN * QTILE;  // stage s: K at +2s*KV, V at +(2s+1)*KV
   static constexpr int BAR_OFF = KV_OFF + NS * 2 * KV;
   static constexpr int SMEM = BAR_OFF + 256 + 6 * 128 * 4 + 1024;
-  // TMEM columns (256 per CTA, two CTAs per SM): S buffers, O, P (bf16 pairs)
-  static constexpr int SB = (HD + (SPLIT ? 64 : 32) + 2 * ATT_K <= 256) ? 2 : 1;
+  // TMEM columns (256 per CTA, two CTAs per SM): two S buffers of 64 columns,
+  // then O.  P(g) (bf16 pairs: hi in columns 0-31, lo in 32-63) overwrites
+  // S(g) in its own buffer, so P is double-buffered along with S.
+  static constexpr int SB = 2;
   static constexpr uint32_t T_O = SB * ATT_K;
-  static constexpr uint32_t T_P = T_O + HD;               // P hi: 32 columns (64 keys)
-  static constexpr uint32_t T_PLO = T_P + ATT_K / 2;      // P lo (split)
   static constexpr uint32_t TMEM_COLS = 256;
-  static_assert(T_PLO + (SPLIT ? ATT_K / 2 : 0) <= TMEM_COLS, "TMEM budget");
+  static_assert(T_O + HD <= TMEM_COLS, "TMEM budget");
 };
 
 __device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
@@ -899,15 +899,7 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
 // issues TMA and tcgen05.mma; the two sides meet only on mbarriers.  P goes
 // to TMEM (tcgen05.st) and is the A operand of P.V straight from there, so
 // a CTA needs no P staging in shared memory: two CTAs per SM.
-// p1 is a compile-time 0 in one-pass mode: `g >= p1` and friends fold away
-#pragma nv_diag_suppress 186
 constexpr int ATT_SOFT = 256;
-// 1: one pass over the key tiles with an online softmax (lazy O rescale);
-// 0: pass 1 takes the exact row max from Qhi.Khi, pass 2 computes P and P.V
-#ifndef ZO2_ATTN_ONEPASS
-#define ZO2_ATTN_ONEPASS 1
-#endif
-constexpr bool ATT_ONEPASS = ZO2_ATTN_ONEPASS != 0;
 // online softmax: the running max moves only when a row's tile max exceeds it
 // by more than 2^ATT_TAU (P values stay <= 2^ATT_TAU, O is rescaled rarely)
 constexpr float ATT_TAU = 8.0f;
@@ -921,30 +913,28 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t *bar_kv = (uint64_t *)(smem + C::BAR_OFF);  // [NS] tile loaded (TMA)
   uint64_t *bar_s = bar_kv + NS;                       // [SB] S written (MMA commit)
-  uint64_t *bar_sfree = bar_s + 2;                     // [SB] S read (256 arrivals)
-  uint64_t *bar_p = bar_sfree + 2;                     // P written to TMEM (256 arrivals)
-  uint64_t *bar_o = bar_p + 1;                         // P.V done (MMA commit)
+  uint64_t *bar_p = bar_s + SB;                        // [SB] P written into its S buffer (256 arrivals)
+  uint64_t *bar_o = bar_p + SB;                        // P.V done (MMA commit)
   uint64_t *bar_kvfree = bar_o + 1;                    // [NS] ring stage read by its MMAs
-  uint32_t *tmem_slot = (uint32_t *)(bar_kvfree + NS);
+  uint64_t *bar_done = bar_kvfree + NS;                // every P.V done (one phase)
+  uint32_t *tmem_slot = (uint32_t *)(bar_done + 1);
   float *xch = (float *)(smem + C::BAR_OFF + 256);     // [2][2][128] row max, then [2][128] row sum
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // heavy (late) query tiles first
   const uint32_t qt = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
   const int row0 = (int)(b * a.seq + qt * ATT_Q);
   const uint32_t n_kt = (qt + 1) * (ATT_Q / ATT_K);  // causal: key tiles up to the diagonal
-  const uint32_t p1 = ATT_ONEPASS ? 0u : n_kt;        // pass-1 tiles (K only, row max)
-  const uint32_t n_all = p1 + n_kt;                  // then n_kt tiles of S, P and P.V
   const uint32_t d = a.dim;
 
   if (threadIdx.x == ATT_SOFT) {
     for (int i = 0; i < NS; ++i) mbar_init(&bar_kv[i], 1);
     for (int i = 0; i < SB; ++i) {
       mbar_init(&bar_s[i], 1);
-      mbar_init(&bar_sfree[i], ATT_SOFT);
+      mbar_init(&bar_p[i], ATT_SOFT);
     }
-    mbar_init(bar_p, ATT_SOFT);
     mbar_init(bar_o, 1);
     for (int i = 0; i < NS; ++i) mbar_init(&bar_kvfree[i], 1);
+    mbar_init(bar_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int p = 0; p < C::PL; ++p) {
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.tq[p]) : "memory");
@@ -963,21 +953,29 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
   const uint32_t tmem = *tmem_slot;
   const uint32_t t_o = tmem + C::T_O;
 
+  // Barrier phases.  Every wait below is on a phase that cannot be two ahead
+  // of it (a parity wait trailing its barrier by two phases would hang):
+  //   bar_s[g%2] phase g/2: S(g+2) is issued only after P.V(g) completed,
+  //     which needs P(g), which the softmax writes after reading S(g);
+  //   bar_p[g%2] phase g/2: P(g+2) needs S(g+2), issued after the MMA thread
+  //     saw P(g) (P.V(g) issued) and P.V(g) completed;
+  //   bar_o phase j, waited at tile j+1 (softmax, only to rescale O) and
+  //     before S(j+2) (MMA thread): P.V(j-1) is complete by then (S(j+1)
+  //     waited for it) and P.V(j+1) needs P(j+1), not yet written.  The
+  //     epilogue cannot wait on bar_o (P.V(n-2) may still run, so a parity
+  //     wait for phase n-1 could be satisfied by phase n-3): it waits for
+  //     bar_done, committed once after the last P.V.
   if (warp == ATT_SOFT / 32) {
     // ================================================ TMA + MMA issue (one thread)
     if (lane == 0) {
       const uint32_t sq = smem_u32(smem + C::Q_OFF), skv = smem_u32(smem + C::KV_OFF);
       auto load_tile = [&](uint32_t g) {
-        const uint32_t j = g < p1 ? g : g - p1;
-        const bool with_v = g >= p1, with_q = g == 0;
+        const bool with_q = g == 0;
         const int st = (int)(g % NS);
-        // pass 1 only needs the max of S, taken from Qhi Khi: K's lo plane stays home
-        const int kpl = with_v ? C::PL : 1;
-        const uint32_t bytes = (uint32_t)(C::KV / C::PL) * (uint32_t)kpl +
-                               (with_v ? (uint32_t)C::KV : 0u) +
+        const uint32_t bytes = 2u * (uint32_t)C::KV +
                                (with_q ? (uint32_t)(C::PL * C::PAN * C::QTILE) : 0u);
         mbar_expect_tx(&bar_kv[st], bytes);
-        const int krow = (int)(b * a.seq + j * ATT_K);
+        const int krow = (int)(b * a.seq + g * ATT_K);
         uint8_t *kb = smem + C::KV_OFF + 2 * st * C::KV;
         for (int p = 0; p < C::PL; ++p)
           for (int c = 0; c < C::PAN; ++c) {
@@ -985,14 +983,12 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
             if (with_q)
               tma_load_2d(smem + C::Q_OFF + (p * C::PAN + c) * C::QTILE, &a.tq[p], &bar_kv[st],
                           (int)(h * HD + 64 * c), row0);
-            if (p < kpl)
-              tma_load_2d(kb + o, &a.tk[p], &bar_kv[st], (int)(d + h * HD + 64 * c), krow);
-            if (with_v)
-              tma_load_2d(kb + C::KV + o, &a.tk[p], &bar_kv[st],
-                          (int)(2 * d + h * HD + 64 * c), krow);
+            tma_load_2d(kb + o, &a.tk[p], &bar_kv[st], (int)(d + h * HD + 64 * c), krow);
+            tma_load_2d(kb + C::KV + o, &a.tk[p], &bar_kv[st], (int)(2 * d + h * HD + 64 * c),
+                        krow);
           }
       };
-      // S[g % SB] = Q K(g)^T (3 passes split in pass 2); K-major A and B
+      // S[g % SB] = Q K(g)^T (3 passes split); K-major A and B
       auto issue_qk = [&](uint32_t g) {
         constexpr uint32_t id = idesc_bf16_b(ATT_K, false);
         const uint32_t ts = tmem + (g % SB) * ATT_K;
@@ -1002,63 +998,59 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
           const uint32_t ko = (uint32_t)((ks / 4) * C::KTILE + (ks % 4) * 32);
           const uint64_t qa = sw128_desc(sq + qo), kd = sw128_desc(sk + ko);
           tc_mma(ts, qa, kd, id, ks != 0);
-          if (SPLIT && g >= p1) {  // pass 1 (row max only): Qhi Khi suffices
+          if (SPLIT) {
             tc_mma(ts, qa, sw128_desc(sk + C::PAN * C::KTILE + ko), id, 1u);
             tc_mma(ts, sw128_desc(sq + C::PAN * C::QTILE + qo), kd, id, 1u);
           }
         }
         tc_commit(&bar_s[g % SB]);
       };
-      // O += P(j) V(j): A = P [128 q x 64 keys] in TMEM, B = V [64 keys x hd] MN-major
+      // O += P(g) V(g): A = P [128 q x 64 keys] in S buffer g % SB (hi columns
+      // 0-31, lo 32-63), B = V [64 keys x hd] MN-major
       auto issue_pv = [&](uint32_t g) {
-        const uint32_t j = g - p1;
         constexpr uint32_t id = idesc_bf16_b(HD, true);
         constexpr uint32_t vlbo = (uint32_t)C::KTILE;  // next 64 hd columns: next panel
         const uint32_t sv = skv + (uint32_t)((2 * (int)(g % NS) + 1) * C::KV);
+        const uint32_t tp = tmem + (g % SB) * ATT_K;
         for (int ks = 0; ks < ATT_K / 16; ++ks) {
           const uint32_t voff = (uint32_t)(ks * 16 * 128);  // 16 keys x 128 B
-          const uint32_t pa = tmem + C::T_P + (uint32_t)(ks * 8);  // 16 keys = 8 columns
+          const uint32_t pa = tp + (uint32_t)(ks * 8);       // 16 keys = 8 columns
           const uint64_t vb = sw128_desc_mn(sv + voff, vlbo);
-          tc_mma_ts(t_o, pa, vb, id, (j | (uint32_t)ks) != 0);
+          tc_mma_ts(t_o, pa, vb, id, (g | (uint32_t)ks) != 0);
           if (SPLIT) {
             tc_mma_ts(t_o, pa, sw128_desc_mn(sv + C::PAN * C::KTILE + voff, vlbo), id, 1u);
-            tc_mma_ts(t_o, tmem + C::T_PLO + (uint32_t)(ks * 8), vb, id, 1u);
+            tc_mma_ts(t_o, pa + ATT_K / 2, vb, id, 1u);
           }
         }
         tc_commit(bar_o);
       };
 
-      for (uint32_t g = 0; g < (uint32_t)NS && g < n_all; ++g) load_tile(g);
+      for (uint32_t g = 0; g < (uint32_t)NS && g < n_kt; ++g) load_tile(g);
       mbar_wait(&bar_kv[0], 0);
       tc_fence_after();
       issue_qk(0);
-      if (p1 > 0) tc_commit(&bar_kvfree[0]);
-      for (uint32_t g = 0; g < n_all; ++g) {
-        // refill the ring stage of tile g - 1 (consumed by S(g - 1) / P.V(g - 1))
-        if (g >= 1 && g - 1 + NS < n_all) {
+      for (uint32_t g = 0; g < n_kt; ++g) {
+        // refill the ring stage of tile g - 1 (read by S(g - 1) and P.V(g - 1))
+        if (g >= 1 && g - 1 + NS < n_kt) {
           const uint32_t gp = g - 1;
-          // a barrier per ring stage (committed after the last MMA reading it):
-          // its next phase belongs to tile gp + NS, loaded right here
           mbar_wait(&bar_kvfree[gp % NS], (gp / NS) & 1u);
           load_tile(gp + NS);
         }
-        // S(g + 1) next: needs K(g + 1) and its S buffer drained (tile g + 1 - SB)
-        if (g + 1 < n_all) {
+        // S(g + 1) next: needs K(g + 1) and its buffer free of P(g - 1)
+        if (g + 1 < n_kt) {
           const uint32_t gn = g + 1;
           mbar_wait(&bar_kv[gn % NS], (gn / NS) & 1u);
-          if (gn >= (uint32_t)SB) mbar_wait(&bar_sfree[gn % SB], ((gn - SB) / SB) & 1u);
+          if (gn >= (uint32_t)SB) mbar_wait(bar_o, (gn - SB) & 1u);
           tc_fence_after();
           issue_qk(gn);
-          if (gn < p1) tc_commit(&bar_kvfree[gn % NS]);  // pass 1: K read by S only
         }
-        if (g >= p1) {  // P.V of this tile once the softmax stored P(j)
-          const uint32_t j = g - p1;
-          mbar_wait(bar_p, j & 1u);
-          tc_fence_after();
-          issue_pv(g);
-          tc_commit(&bar_kvfree[g % NS]);
-        }
+        // P.V(g) once the softmax stored P(g)
+        mbar_wait(&bar_p[g % SB], (g / SB) & 1u);
+        tc_fence_after();
+        issue_pv(g);
+        tc_commit(&bar_kvfree[g % NS]);
       }
+      tc_commit(bar_done);
     }
   } else {
     // ================================================ softmax warps
@@ -1066,44 +1058,30 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
     const int r = quad * 32 + lane;  // query row within the tile (TMEM lane)
     const int c0 = 32 * half;        // this warp's 32 columns of S
-    float mrow = -INFINITY, mscaled = ATT_ONEPASS ? -INFINITY : 0.f, lsum = 0.f;
-    for (uint32_t g = 0; g < n_all; ++g) {
-      const bool pass2 = ATT_ONEPASS || g >= p1;
-      const uint32_t j = pass2 ? g - p1 : g;
-      const int lim = (int)(qt * ATT_Q) + r - (int)(j * ATT_K) - c0;  // visible: i <= lim
+    float mscaled = -INFINITY, lsum = 0.f;
+    for (uint32_t g = 0; g < n_kt; ++g) {
+      const int lim = (int)(qt * ATT_Q) + r - (int)(g * ATT_K) - c0;  // visible: i <= lim
+      const uint32_t ts = tmem + (g % SB) * ATT_K;
       mbar_wait(&bar_s[g % SB], (g / SB) & 1u);
       tc_fence_after();
       uint32_t v[32];
-      tmem_ld32(tmem + (g % SB) * ATT_K + lane_base + (uint32_t)c0, v);
-      tc_fence_before();
-      mbar_arrive(&bar_sfree[g % SB]);
-      if (!pass2) {
+      tmem_ld32(ts + lane_base + (uint32_t)c0, v);
+      float mt = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (i <= lim) mrow = fmaxf(mrow, __uint_as_float(v[i]));
-        if (g + 1 == n_kt) {
-          xch[half * 128 + r] = mrow;
-          asm volatile("bar.sync 1, %0;" ::"n"(ATT_SOFT) : "memory");
-          mscaled = fmaxf(xch[r], xch[128 + r]) * a.scale_log2;
-        }
-        continue;
-      }
-      float alpha = 1.f;  // O and l rescale of this row (online softmax)
-      if (ATT_ONEPASS) {
-        float mt = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (i <= lim) mt = fmaxf(mt, __uint_as_float(v[i]));
-        // the two warps of a quadrant hold the halves of the same rows
-        float *slot = xch + (j & 1u) * 256;
-        slot[half * 128 + r] = mt;
-        asm volatile("bar.sync %0, 64;" ::"r"(2 + quad) : "memory");
-        mt = fmaxf(slot[r], slot[128 + r]) * a.scale_log2;
-        if (mt > mscaled + ATT_TAU) {
-          alpha = ex2f(mscaled - mt);
-          mscaled = mt;
-          lsum *= alpha;
-        }
+      for (int i = 0; i < 32; ++i)
+        if (i <= lim) mt = fmaxf(mt, __uint_as_float(v[i]));
+      // the two warps of a quadrant hold the halves of the same rows; the
+      // barrier also orders both warps' S reads before either overwrites the
+      // buffer with P
+      float *slot = xch + (g & 1u) * 256;
+      slot[half * 128 + r] = mt;
+      asm volatile("bar.sync %0, 64;" ::"r"(2 + quad) : "memory");
+      mt = fmaxf(slot[r], slot[128 + r]) * a.scale_log2;
+      float alpha = 1.f;  // O and l rescale of this row
+      if (mt > mscaled + ATT_TAU) {
+        alpha = ex2f(mscaled - mt);
+        mscaled = mt;
+        lsum *= alpha;
       }
       float pv[32];
 #pragma unroll
@@ -1123,35 +1101,33 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
           lo[e] = *reinterpret_cast<const uint32_t *>(&lv);
         }
       }
-      // P(j) replaces P(j - 1) in TMEM once P.V(j - 1) has read it
-      if (j >= 1) {
-        mbar_wait(bar_o, (j - 1) & 1u);
+      // a row's max moved: O(g - 1) must be final before it is rescaled (and
+      // P.V(g) is not issued before this warp's P(g) arrives)
+      if (g >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        mbar_wait(bar_o, (g - 1) & 1u);
         tc_fence_after();
-        // O(j - 1) is final: rescale this warp's O columns if any row's max moved
-        if (ATT_ONEPASS && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll 1
-          for (int o0 = half * (HD / 2); o0 < (half + 1) * (HD / 2); o0 += 32) {
-            uint32_t w[32];
-            tmem_ld32(t_o + lane_base + (uint32_t)o0, w);
+        for (int o0 = half * (HD / 2); o0 < (half + 1) * (HD / 2); o0 += 32) {
+          uint32_t w[32];
+          tmem_ld32(t_o + lane_base + (uint32_t)o0, w);
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              uint32_t x[16];
+          for (int q = 0; q < 2; ++q) {
+            uint32_t x[16];
 #pragma unroll
-              for (int e = 0; e < 16; ++e) x[e] = __float_as_uint(__uint_as_float(w[16 * q + e]) * alpha);
-              tmem_st16(t_o + lane_base + (uint32_t)(o0 + 16 * q), x);
-            }
+            for (int e = 0; e < 16; ++e) x[e] = __float_as_uint(__uint_as_float(w[16 * q + e]) * alpha);
+            tmem_st16(t_o + lane_base + (uint32_t)(o0 + 16 * q), x);
           }
         }
       }
-      tmem_st16(tmem + C::T_P + lane_base + (uint32_t)(c0 / 2), hi);
-      if (SPLIT) tmem_st16(tmem + C::T_PLO + lane_base + (uint32_t)(c0 / 2), lo);
+      tmem_st16(ts + lane_base + (uint32_t)(c0 / 2), hi);
+      if (SPLIT) tmem_st16(ts + lane_base + (uint32_t)(ATT_K / 2 + c0 / 2), lo);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
-      mbar_arrive(bar_p);
+      mbar_arrive(&bar_p[g % SB]);
     }
     // ---------------------------------------------- epilogue: O / l -> bf16 planes
     xch[512 + half * 128 + r] = lsum;
-    mbar_wait(bar_o, (n_kt - 1) & 1u);  // last P.V (and so every P.V) done
+    mbar_wait(bar_done, 0);  // every P.V done
     tc_fence_after();
     asm volatile("bar.sync 1, %0;" ::"n"(ATT_SOFT) : "memory");
     const float inv = 1.0f / (xch[512 + r] + xch[640 + r]);
