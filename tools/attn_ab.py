@@ -9,7 +9,11 @@ from paper_2503_12668_b200 import _lib  # noqa: E402
 
 import os
 _lib.call("zo2_set_attention_variant", int(os.environ.get("ZO2_ATTN_VARIANT", "0")))
-for B, S, H, hd, split in ((16, 512, 32, 64, True), (16, 512, 32, 128, False)):
+SHAPES = ((16, 512, 32, 64, True), (16, 512, 32, 128, False))
+if os.environ.get("ATTN_SHAPES"):  # e.g. "4,2048,32,64,1;16,512,32,64,1"
+    SHAPES = tuple(tuple(int(x) for x in t.split(",")) for t in os.environ["ATTN_SHAPES"].split(";"))
+for B, S, H, hd, split in SHAPES:
+    split = bool(split)
     d = H * hd
     T = B * S
     qh = torch.randn(T, 3 * d, device="cuda").to(torch.bfloat16)
