@@ -420,6 +420,47 @@ def test_attention(cuda, B, S, H, hd, split):
     assert (got - ref).abs().max().item() < tol * max(1.0, ref.abs().max().item())
 
 
+def _attention_ref(qh, ql, B, S, H, hd, cuda):
+    d = H * hd
+    src = (qh.double() + ql.double()) if ql is not None else qh.double()
+    q, k, v = (t.reshape(B, S, H, hd).transpose(1, 2) for t in src.split(d, -1))
+    sc = q @ k.transpose(-1, -2) / hd ** 0.5
+    mask = torch.tril(torch.ones(S, S, dtype=torch.bool, device=cuda))
+    sc = sc.masked_fill(~mask, float("-inf"))
+    return (torch.softmax(sc, -1) @ v).transpose(1, 2).reshape(B * S, d)
+
+
+@pytest.mark.parametrize("B,S,H,hd,split", [(1, 512, 2, 64, True), (1, 512, 2, 128, False),
+                                            (1, 2048, 2, 64, True)])
+@pytest.mark.parametrize("trend", ["rising", "falling"])
+def test_attention_online_softmax_rescale(cuda, B, S, H, hd, split, trend):
+    """Scores that grow (or shrink) along the key axis: with 'rising' every
+    later key tile raises the row maximum far beyond 2^8, so the tcgen05
+    kernel's lazy O rescale runs on most tiles; 'falling' keeps tile 0's
+    maximum.  Both must match the fp64 reference like random inputs do."""
+    d = H * hd
+    g = torch.Generator(device=cuda).manual_seed(3)
+    u = torch.randn(H, hd, device=cuda, generator=g) / hd ** 0.25
+    pos = torch.arange(S, device=cuda, dtype=torch.float32)
+    ramp = (pos / 16.0) if trend == "rising" else (S - pos) / 16.0
+    q = u.expand(B * S, H, hd).reshape(B * S, d).clone()
+    k = (u[None] * ramp.repeat(B)[:, None, None]).reshape(B * S, d)
+    v = torch.randn(B * S, d, device=cuda, generator=g)
+    qkv = torch.cat([q, k, v], -1) + 0.01 * torch.randn(B * S, 3 * d, device=cuda, generator=g)
+    qh = qkv.to(torch.bfloat16)
+    ql = (qkv - qh.float()).to(torch.bfloat16) if split else None
+    hi = torch.empty(B * S, d, dtype=torch.bfloat16, device=cuda)
+    lo = torch.empty_like(hi) if split else None
+    L().call("zo2_attention", qh.data_ptr(), ql.data_ptr() if split else None, B, S, H, hd,
+             hi.data_ptr(), lo.data_ptr() if split else None, stream())
+    torch.cuda.synchronize()
+    ref = _attention_ref(qh, ql, B, S, H, hd, cuda)
+    got = hi.double() + (lo.double() if split else 0)
+    tol = 5e-5 if split else 2e-2
+    assert torch.isfinite(got).all()
+    assert (got - ref).abs().max().item() < tol * max(1.0, ref.abs().max().item())
+
+
 def test_embed_dual_matches_oracle(cuda, oracle):
     from paper_2503_12668_b200.model import ModelSpec
     spec = ModelSpec(1, 32, 4, 64, 16)
