@@ -16,9 +16,15 @@ def main(path, steps):
         k = r[name_i].split("(")[0][:70]
         t[k] += float(r[val_i]) / 1e6
         n[k] += 1
-    tot = sum(t.values())
+    # parameter initialisation (init_params before the first step) is not
+    # part of any step: listed apart, out of the shares
+    setup = {k for k in t if "k_init_normal" in k}
+    tot = sum(v for k, v in t.items() if k not in setup)
     for k, v in t.most_common():
-        print(f"{v / steps:9.2f} ms/step {100 * v / tot:5.1f}%  n={n[k]:5d}  {k}")
+        if k not in setup:
+            print(f"{v / steps:9.2f} ms/step {100 * v / tot:5.1f}%  n={n[k]:5d}  {k}")
+    for k in setup:
+        print(f"{t[k]:9.2f} ms total (setup, not a step)  n={n[k]:5d}  {k}")
 
 
 if __name__ == "__main__":
