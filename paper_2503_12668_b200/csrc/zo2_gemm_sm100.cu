@@ -30,6 +30,11 @@ void zo2_count_launch(uint64_t n = 1);
 #ifndef ZO2_GEMM_SMEM_KB
 #define ZO2_GEMM_SMEM_KB 200  // operand staging budget per CTA
 #endif
+// Smaller budgets (2 split / 5 bf16 stages, leaving room for two K2 CTAs
+// beside a GEMM CTA) pass the GEMM tests alone but hung in the full step with
+// K2 running concurrently (tools/ab_variants.sh, cfg3); until that is
+// understood only the tested budget is accepted.
+static_assert(ZO2_GEMM_SMEM_KB >= 192, "GEMM staging budgets below 192 KB are not supported");
 
 namespace {
 
