@@ -148,3 +148,32 @@ def test_cross_step_edges_keep_every_hazard(n, k, sets):
         dur = {t.key: (5.0 if t.lane is Lane.COMPUTE else 1.0) for t in two.tasks}
         ev = _simulate(two, lambda t: dur[t.key]).by_key()
         assert ev[tag(ukey(blocks[0]), 1)].t_start < ev[tag(ckey(head), 0)].t_end
+
+
+def test_operand_set_choice_follows_capacity():
+    """Host logic of Zo2Engine._choose_operand_sets (CPU): two operand sets
+    unless the device capacity only admits one; explicit choices are kept."""
+    from types import SimpleNamespace
+
+    from paper_2503_12668_b200.engine import Zo2Engine
+    from paper_2503_12668_b200.model import DualForward, ModelSpec
+    spec = ModelSpec(2, 64, 4, 96, 32)
+    one = DualForward.estimate_nbytes(spec, 4, "f32", 1)
+    two = DualForward.estimate_nbytes(spec, 4, "f32", 2)
+    assert two > one > 0
+    calls = []
+
+    def fake(cap, auto=True, used=1000):
+        eng = SimpleNamespace(
+            _sets_auto=auto, operand_sets=2,
+            dev=SimpleNamespace(fwd=None, operand_sets=2),
+            runtime=SimpleNamespace(pool=SimpleNamespace(used=used, capacity=cap)),
+            workload=SimpleNamespace(spec=spec, arith="f32"),
+            _set_k2_grid=lambda: calls.append(1))
+        Zo2Engine._choose_operand_sets(eng, 4)
+        return eng.operand_sets, eng.dev.operand_sets
+    assert fake(float("inf")) == (2, 2)
+    assert fake(1000 + two) == (2, 2)
+    assert fake(1000 + two - 1) == (1, 1)
+    assert fake(1000 + one) == (1, 1)
+    assert fake(1000 + one, auto=False) == (2, 2)
