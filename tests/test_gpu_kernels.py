@@ -228,6 +228,53 @@ def test_update_perturb_block_scale_matches_axpy_chain(cuda, fmt):
     assert torch.equal(op.hi.view(-1), wq.view(-1).to(torch.bfloat16))
 
 
+@pytest.mark.parametrize("dim,codec", [(7168, "bf16"), (12288, "f16")])
+def test_update_perturb_full_size_codec_block(cuda, dim, codec):
+    """BASELINE sizes: one whole OPT-30B block (616.7 M parameters, bf16 wire,
+    cfg4) and one OPT-175B block (1.81 G parameters, f16 wire, cfg5) through
+    K2 on the codec arena -- decode, deferred update, +eps/-2eps/+eps,
+    encode, bf16 operands -- against decode -> four reference-order passes
+    of zo2_axpy_z in f32 -> encode.  Bit-identical arena and W+ operand."""
+    from paper_2503_12668_b200.model import (DualForward, ModelSpec, block_layout, module_size,
+                                             segments)
+    _l = L()
+    spec = ModelSpec(1, dim, dim // 128, 50272, 512)
+    fwd = DualForward(spec, 1, "bf16", cuda, 1)
+    n = module_size(spec, "block.0")
+    base, lrs, rs, eps, lr, g = 30_000_000_000, 0x5EED, 0xBEEF, 1e-3, 1e-7, -2.5
+    tdt = torch.bfloat16 if codec == "bf16" else torch.float16
+    fmt = _l.BF16 if codec == "bf16" else _l.F16
+    gen = torch.Generator(device=cuda).manual_seed(11)
+    arena = torch.empty(n, dtype=tdt, device=cuda)
+    for i in range(0, n, 1 << 28):  # chunked init: no n-sized f32 temporary
+        j = min(n, i + (1 << 28))
+        arena[i:j] = (torch.randn(j - i, device=cuda, generator=gen) * 0.02).to(tdt)
+    ref = arena.float()
+    d_g = torch.tensor([g], dtype=torch.float64, device=cuda)
+    counts = torch.zeros(2, dtype=torch.int64, device=cuda)
+    descs = fwd.block_descs(0)
+    _l.call("zo2_update_perturb", arena.data_ptr(), fmt, n, base, 1, d_g.data_ptr(), lr, lrs,
+            1, eps, rs, descs, len(descs), counts.data_ptr(), stream())
+
+    def axpy(coef, seed):
+        _l.call("zo2_axpy_z", ref.data_ptr(), _l.F32, n, coef, seed, 0, base, stream())
+
+    qkv = [sg for sg in segments(block_layout(spec)) if sg.name == "qkv_w"][0]
+    axpy(-(lr * g), lrs)
+    axpy(eps, rs)
+    wq = ref[qkv.offset: qkv.offset + qkv.size].view(qkv.shape).t().contiguous()
+    axpy(-2.0 * eps, rs)
+    axpy(eps, rs)
+    torch.cuda.synchronize()
+    enc = ref.to(tdt)
+    del ref
+    bad = (arena.view(torch.int16) != enc.view(torch.int16)).nonzero().flatten()
+    assert bad.numel() == 0, f"{bad.numel()} of {n} differ, first {bad[:5].tolist()}"
+    assert counts.cpu().tolist() == [0, 0]
+    op = fwd.sets[0][1]["qkv_w"][0]
+    assert torch.equal(op.hi.view(-1), wq.view(-1).to(torch.bfloat16))
+
+
 # ------------------------------------------------------------------ K9
 @pytest.mark.parametrize("fmt", ["bf16", "f16", "f8"])
 def test_codecs_bit_exact(cuda, golden, fmt):
