@@ -16,9 +16,10 @@ def main(path, steps):
         k = r[name_i].split("(")[0][:70]
         t[k] += float(r[val_i]) / 1e6
         n[k] += 1
-    # parameter initialisation (init_params before the first step) is not
-    # part of any step: listed apart, out of the shares
-    setup = {k for k in t if "k_init_normal" in k}
+    # parameter initialisation (init_params before the first step: random
+    # init, and the codec encode of the host masters) is not part of any
+    # step: listed apart, out of the shares
+    setup = {k for k in t if "k_init_normal" in k or "k_encode" in k}
     tot = sum(v for k, v in t.items() if k not in setup)
     for k, v in t.most_common():
         if k not in setup:
