@@ -24,7 +24,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import NonFiniteLossError, SchedulingContractError, StateCorruptionError
+from .errors import (NonFiniteLossError, SchedulingContractError, StateCorruptionError,
+                     UsageError)
 from .model import (EMBED_ID, HEAD_ID, DualForward, ModelSpec, module_order, module_size,
                     rng_offsets)
 from .numerics import BATCH_STREAM, PERTURB_STREAM, RngState, derive_step_seed, raw_uint64
@@ -314,9 +315,19 @@ class Zo2Engine:
         import torch.distributed as dist
         self.dist_group = group or dist.group.WORLD
         self.world = dist.get_world_size(self.dist_group)
+        sharded = False
         if shard_transfers and not getattr(self.runtime, "resident", False):
-            return self.runtime.enable_sharding(dist.get_rank(self.dist_group), self.world)
-        return False
+            sharded = self.runtime.enable_sharding(dist.get_rank(self.dist_group), self.world)
+        params = getattr(self.runtime, "params", None)
+        if self.world > 1 and getattr(params, "shared_masters", False) and not sharded:
+            # every rank would upload and offload whole blocks of one shared
+            # copy: a rank running ahead would hand the next one already
+            # updated weights.  One writer per byte needs sharded transfers.
+            raise UsageError("node-shared host masters need sharded transfers "
+                             "(enable_data_parallel(shard_transfers=True), block size "
+                             "divisible by the world size and a working in-place "
+                             "all-gather); use per-rank masters otherwise")
+        return sharded
 
     # -- bookkeeping of one module visit (zo2_engine.py:187-203) -------------
     def _visit(self, module: str, step: int) -> tuple[RngState, RngState | None, bool]:
@@ -582,6 +593,13 @@ class Zo2Engine:
     def finalize(self) -> ModelParams:
         """Drain the last pending update (zo2_engine.py:318-336); idempotent."""
         rt = self.runtime
+        shard = getattr(rt, "shard", None)
+        if shard is not None and self.pending.valid:
+            # node-shared masters: every rank's last offloads must have landed
+            # before any rank reads a whole block back
+            import torch.distributed as dist
+            torch.cuda.synchronize(rt.device)
+            dist.barrier(group=shard[2])
         if self.pending.valid:
             _lib.call("zo2_set_rng_mode", RNG_MODES[self.rng])
             comp = self.lanes[Lane.COMPUTE]
@@ -604,12 +622,24 @@ class Zo2Engine:
                     self._k2(rt.slots[slot], rt.wire_fmt.code, module, 1, lrs.seed, False, 0,
                              descs, comp)
                     with torch.cuda.stream(comp):
-                        rt.host[module].copy_(rt.slots[slot], non_blocking=True)
+                        if shard is None:
+                            rt.host[module].copy_(rt.slots[slot], non_blocking=True)
+                        else:
+                            # write back only this rank's shard: another rank
+                            # may already have updated its own shard in the
+                            # shared master, so the rest of this copy may hold
+                            # a twice-updated region
+                            lo, hi = shard[3], shard[4]
+                            rt.host[module][lo:hi].copy_(rt.slots[slot][lo:hi],
+                                                         non_blocking=True)
                     comp.synchronize()
                 else:
                     self._k2(rt.persistent[module], _lib.F32, module, 1, lrs.seed, False, 0,
                              descs, comp)
             comp.synchronize()
+            if shard is not None:
+                import torch.distributed as dist
+                dist.barrier(group=shard[2])  # all shards written before export
         self.pending.clear()
         self.mgr.rsb.clear()
         self._prev_enq = None

@@ -121,6 +121,7 @@ class ModelParams:
             spec, embedding, blocks, lm_head, fmt)
         self.block_codec: ElemFormat | None = None  # blocks already hold wire-format bits
         self.init_conversion = None
+        self.shared_masters = False  # blocks are views of a node-wide SharedHostMasters
 
     def buckets(self) -> list[tuple[str, torch.Tensor]]:
         return ([(EMBED_ID, self.embedding)] +
@@ -241,6 +242,7 @@ def init_params(spec: ModelSpec, state: RngState, fmt: ElemFormat = ElemFormat.F
     p = ModelParams(spec, emb, blocks, head, fmt)
     p.block_codec = cfmt
     p.init_conversion = conv
+    p.shared_masters = host_masters is not None
     return p
 
 
