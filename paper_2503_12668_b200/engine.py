@@ -592,6 +592,8 @@ class Zo2Engine:
 
     def finalize(self) -> ModelParams:
         """Drain the last pending update (zo2_engine.py:318-336); idempotent."""
+        if self._async:  # iterations enqueued by step_async: check them first
+            self.drain()
         rt = self.runtime
         shard = getattr(rt, "shard", None)
         if shard is not None and self.pending.valid:
