@@ -83,3 +83,33 @@ def test_argument_errors_raise_without_gpu():
     with pytest.raises(UsageError):
         _lib.call("zo2_update_perturb", 1, 1, 4, 0, 1, None, 0.1, 0, 1, 1e-3, 0, None, 0,
                   None, None)
+
+
+def test_host_side_controls_without_gpu():
+    """The host-only entry points of the C ABI: version, launch counter, the
+    z-generator switch and the tuning setters with their argument checks."""
+    from paper_2503_12668_b200 import _lib
+    from paper_2503_12668_b200.errors import UsageError
+    lib = _lib.load()
+    assert lib.zo2_version() >= 1
+    n0 = lib.zo2_launch_count()
+    assert lib.zo2_launch_count() == n0  # no device work happens here
+    mode = lib.zo2_rng_mode()
+    try:
+        for m in (1, 0):
+            _lib.call("zo2_set_rng_mode", m)
+            assert lib.zo2_rng_mode() == m
+        with pytest.raises(UsageError):
+            _lib.call("zo2_set_rng_mode", 2)
+        assert b"zo2_set_rng_mode" in lib.zo2_last_error()
+    finally:
+        _lib.call("zo2_set_rng_mode", mode)
+    for fn, good, bad in (("zo2_set_k2_ctas_per_sm", (0, 1, 32), (-1, 33)),
+                          ("zo2_set_attention_variant", (0, 1), (-1, 2)),
+                          ("zo2_set_gemm_variant", (0, 1, 2), (-1, 3))):
+        for v in bad:
+            with pytest.raises(UsageError):
+                _lib.call(fn, v)
+        for v in good:
+            _lib.call(fn, v)
+        _lib.call(fn, good[0])
