@@ -343,19 +343,34 @@ def run_ours(args, cfg, rank, world, local_rank):
                                  host_masters=shm)
     else:
         params = init_params(spec, RngState(SEED), device=dev, codec=cfg["codec"])
-    if cfg.get("resident"):  # MeZO: blocks live in HBM, transfers are no-ops
-        from paper_2503_12668_b200.runtime import ResidentRuntime
-        rt = ResidentRuntime(params, device=dev)
-    else:
-        rt = OffloadRuntime(params, k_slots=cfg["slots"], codec=cfg["codec"],
-                            capacity_bytes=cfg.get("cap", float("inf")), device=dev)
-    eng = Zo2Engine(TransformerWorkload(params, cfg["arith"]),
-                    ZOConfig(EPS, cfg["lr"], max(1, args.steps), SEED), rt, validate=True,
-                    operand_sets=args.operand_sets, rng=args.rng,
-                    pipeline_steps=not args.no_pipeline)
+    def make_engine(params):
+        if cfg.get("resident"):  # MeZO: blocks live in HBM, transfers are no-ops
+            from paper_2503_12668_b200.runtime import ResidentRuntime
+            rt = ResidentRuntime(params, device=dev)
+        else:
+            rt = OffloadRuntime(params, k_slots=cfg["slots"], codec=cfg["codec"],
+                                capacity_bytes=cfg.get("cap", float("inf")), device=dev)
+        eng = Zo2Engine(TransformerWorkload(params, cfg["arith"]),
+                        ZOConfig(EPS, cfg["lr"], max(1, args.steps), SEED), rt, validate=True,
+                        operand_sets=args.operand_sets, rng=args.rng,
+                        pipeline_steps=not args.no_pipeline)
+        return rt, eng
+
+    rt, eng = make_engine(params)
     sharded = False
     if world > 1:
-        sharded = eng.enable_data_parallel(shard_transfers=shm is not None)
+        from paper_2503_12668_b200.errors import UsageError
+        try:
+            sharded = eng.enable_data_parallel(shard_transfers=shm is not None)
+        except UsageError as e:  # shared masters but no sharded transfers
+            print(f"bench: {e}; using per-rank masters", file=sys.stderr)
+            del eng, rt, params
+            dist.barrier()
+            shm.close()
+            shm = None
+            params = init_params(spec, RngState(SEED), device=dev, codec=cfg["codec"])
+            rt, eng = make_engine(params)
+            sharded = eng.enable_data_parallel(shard_transfers=False)
     ds = gen_synthetic(V, S, 64 * world, RngState(SEED), "affine", B)
     from paper_2503_12668_b200.parallel import shard_indices
 

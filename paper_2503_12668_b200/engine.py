@@ -319,7 +319,8 @@ class Zo2Engine:
         if shard_transfers and not getattr(self.runtime, "resident", False):
             sharded = self.runtime.enable_sharding(dist.get_rank(self.dist_group), self.world)
         params = getattr(self.runtime, "params", None)
-        if self.world > 1 and getattr(params, "shared_masters", False) and not sharded:
+        if (self.world > 1 and getattr(params, "shared_masters", False) and not sharded
+                and not getattr(self.runtime, "resident", False)):
             # every rank would upload and offload whole blocks of one shared
             # copy: a rank running ahead would hand the next one already
             # updated weights.  One writer per byte needs sharded transfers.
