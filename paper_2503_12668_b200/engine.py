@@ -273,7 +273,8 @@ class Zo2Engine:
         # whose tail the next one overlaps instead of a full step barrier
         self.pipeline_steps = pipeline_steps
         self._prev_enq = None
-        self._hist = torch.zeros(64, 4, dtype=torch.float64, device=runtime.device)
+        # per-iteration (l+, l-, g, flag) of step_async until drain()
+        self._hist = torch.zeros(1024, 4, dtype=torch.float64, device=runtime.device)
         # data parallel: loss sums are all-reduced before g is formed (K10)
         self.dist_group = None
         self.world = 1
