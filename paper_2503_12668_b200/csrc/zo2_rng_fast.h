@@ -63,7 +63,13 @@ ZO2F_HD float zo2f_as_f32(uint32_t u) {
 }
 
 ZO2F_HD void zo2f_mulhilo32(uint32_t a, uint32_t b, uint32_t *hi, uint32_t *lo) {
+#if defined(__CUDA_ARCH__)
+  /* one IMAD.WIDE.U32; the 64-bit C form left an add of zero per multiply */
+  uint64_t p;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(p) : "r"(a), "r"(b));
+#else
   const uint64_t p = (uint64_t)a * b;
+#endif
   *hi = (uint32_t)(p >> 32);
   *lo = (uint32_t)p;
 }
