@@ -220,6 +220,7 @@ __device__ __forceinline__ void emit4(const zo2_segment_desc &sg, int kind, uint
 
 template <int FMT, bool FAST, bool UPD, bool PERT>
 __device__ __forceinline__ void k2_tiles(void *arena, const K2Table &T, const K2Params &P,
+                                         const ZxKeys2 &KS,
                                          K2Smem<typename Wire<FMT>::A> &sm, unsigned &nn,
                                          unsigned &ns) {
   typedef typename Wire<FMT>::A A;
@@ -311,12 +312,12 @@ __device__ __forceinline__ void k2_tiles(void *arena, const K2Table &T, const K2
     if (cnt > 0) {
       uint64_t r[4];
       if (UPD) {
-        zx_raw4(P.lrs_seed, ZO2_PERTURB_STREAM, P.base + idx, r);
+        zx_raw4_k(KS.lrs, P.base + idx, r);
 #pragma unroll
         for (int j = 0; j < 4; ++j) classify(j, r[j], j < cnt);
       }
       if (PERT) {
-        zx_raw4(P.rs_seed, ZO2_PERTURB_STREAM, P.base + idx, r);
+        zx_raw4_k(KS.rs, P.base + idx, r);
 #pragma unroll
         for (int j = 0; j < 4; ++j) classify(OFF + j, r[j], j < cnt);
       }
@@ -481,6 +482,7 @@ __device__ __forceinline__ double resolve_ucoef(const double *d_g, double lr, in
 
 template <int FMT, bool FAST>
 __global__ void __launch_bounds__(NT, ZO2_K2_MINB) k_update_perturb(void *arena, K2Table T, K2Params P,
+                                                          const __grid_constant__ ZxKeys2 KS,
                                                           const double *d_g, double lr,
                                                           uint64_t *counts) {
   typedef typename Wire<FMT>::A A;
@@ -493,10 +495,10 @@ __global__ void __launch_bounds__(NT, ZO2_K2_MINB) k_update_perturb(void *arena,
   int upd = P.do_update;
   P.ucoef = resolve_ucoef(d_g, lr, upd);
   unsigned nn = 0, ns = 0;
-  if (upd && P.do_perturb) k2_tiles<FMT, FAST, true, true>(arena, T, P, sm, nn, ns);
-  else if (upd) k2_tiles<FMT, FAST, true, false>(arena, T, P, sm, nn, ns);
-  else if (P.do_perturb) k2_tiles<FMT, FAST, false, true>(arena, T, P, sm, nn, ns);
-  else k2_tiles<FMT, FAST, false, false>(arena, T, P, sm, nn, ns);
+  if (upd && P.do_perturb) k2_tiles<FMT, FAST, true, true>(arena, T, P, KS, sm, nn, ns);
+  else if (upd) k2_tiles<FMT, FAST, true, false>(arena, T, P, KS, sm, nn, ns);
+  else if (P.do_perturb) k2_tiles<FMT, FAST, false, true>(arena, T, P, KS, sm, nn, ns);
+  else k2_tiles<FMT, FAST, false, false>(arena, T, P, KS, sm, nn, ns);
   if (FMT != ZO2_F32 && FMT != ZO2_F64) add_counts(counts, nn, ns);
 }
 
@@ -518,7 +520,10 @@ int launch_k2(void *arena, const K2Table &T, const K2Params &P, const double *d_
   if (g_k2_ctas_per_sm && g_k2_ctas_per_sm < per_sm) per_sm = g_k2_ctas_per_sm;
   const uint64_t cap = 148ull * per_sm;
   const unsigned g = (unsigned)(tiles < cap ? tiles : cap);
-  k_update_perturb<FMT, FAST><<<g, NT, 0, s>>>(arena, T, P, d_g, lr, counts);
+  ZxKeys2 KS;
+  zx_round_keys(P.lrs_seed, ZO2_PERTURB_STREAM, KS.lrs);
+  zx_round_keys(P.rs_seed, ZO2_PERTURB_STREAM, KS.rs);
+  k_update_perturb<FMT, FAST><<<g, NT, 0, s>>>(arena, T, P, KS, d_g, lr, counts);
   zo2_count_launch();
   ZO2_CHECK_LAUNCH();
   return ZO2_OK;
