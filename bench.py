@@ -2,15 +2,18 @@
 """ZO2 step throughput on B200 (BASELINE.json metric: "ZO step tokens/s
 (1/2/4/8 B200) vs PCIe/tensor roofline; H2D GB/s; GPU idle %").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl ours|reference]
 
-Workload (default cfg2 = BASELINE configs[1]): OPT-1.3B geometry (24 blocks,
-d 2048, 32 heads, V 50272), per-block offload, f32 parameters and f32 wire,
-batch 16 x 512 synthetic tokens per rank, random-init weights (init_params
-semantics, seed 1).  One "step" = one full ZO2 iteration (dual forward of
-every module with the deferred ZO-SGD update fused in, all 24 blocks
-uploaded and offloaded over PCIe).  Each step streams 4.8 GB of block
-weights per direction, far larger than the 126 MB L2 (no flush needed).
+Workload (default cfg4 = BASELINE configs[3], the north-star target): OPT-30B
+geometry (48 blocks, d 7168, 56 heads, V 50272), per-block offload under an
+18 GB HBM cap, bf16 compute with the bf16 wire codec (the reference's AMP
+mode), batch 16 x 512 synthetic tokens per rank, random-init weights
+(init_params semantics, seed 1), the reference's exact z stream.  One "step"
+= one full ZO2 iteration (dual forward of every module with the deferred
+ZO-SGD update fused in, all 48 blocks uploaded and offloaded over PCIe).
+Each step streams 59 GB of block weights per direction, far larger than the
+126 MB L2 (no flush needed).  --config cfg2 (OPT-1.3B, f32 parameters and
+wire, bf16x3 split GEMMs) and the others are the secondary lines.
 
 value  device-timed (CUDA events, compute stream, max over ranks) with the
        batch already resident in HBM, steps enqueued asynchronously.
@@ -490,14 +493,18 @@ def run_ours(args, cfg, rank, world, local_rank):
         "metric": "ZO step tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32" if split else "bf16", "data": "synthetic",
+        "dtype": "bf16x3" if split else "bf16", "data": "synthetic",
         "config": {"workload": cfg["workload"], "model": f"OPT geometry {nb}x{d}, V={V}",
                    "global_batch": B * world, "seq_len": S,
                    "parallelism": (f"dp{world}" + (" (shared masters, sharded PCIe + NVLink "
                                                    "all-gather)" if sharded else "")
                                    if world > 1 else "single"),
                    "wire": cfg["codec"] if cfg["codec"] != "none" else "f32",
-                   "compute": "3-pass bf16 split GEMM (f32-faithful)" if split else "bf16 GEMM",
+                   "compute": ("f32 parameters / update / LN / CE; GEMMs as bf16x3 splits "
+                               "(hi*hi + hi*lo + lo*hi, ~16-bit operand mantissas, f32 "
+                               "accumulate)" if split else
+                               "bf16 GEMM operands, f32 accumulate; f32 parameters / update / "
+                               "LN / softmax / residual, CE in f64"),
                    "l2": "inputs larger than L2 (4.8+ GB of weights streamed per step)",
                    "rng": args.rng + (" (reference z stream, bit-exact)" if args.rng == "exact"
                                       else " (Philox4x32 + binary32 erfinv, not the reference's z)"),
@@ -537,6 +544,15 @@ def run_ours(args, cfg, rank, world, local_rank):
                 "d2h_bytes_per_step": 4 * 8 + wire_per_dir,
                 "note": "h2d/d2h include the per-step block weight traffic of the offload"},
         "gpu_launches": int(launches),
+        "device_memory": {"max_memory_allocated_bytes": int(torch.cuda.max_memory_allocated(dev)),
+                          "max_memory_reserved_bytes": int(torch.cuda.max_memory_reserved(dev)),
+                          "cap_bytes": cfg.get("cap"),
+                          "pool_peak_bytes": int(rt.pool.peak_used),
+                          "under_cap": (torch.cuda.max_memory_reserved(dev) <= cfg["cap"]
+                                        if cfg.get("cap") else None),
+                          "note": "torch caching-allocator peaks over the whole run (all "
+                                  "device tensors: arenas, operands, activations, masters of "
+                                  "the resident modules)"},
         "clocks": clk.summary(),
         **({"full_depth_extrapolation": full_depth_estimate(tls, cfg, T * world)}
            if cfg.get("full_blocks") else {}),
@@ -564,7 +580,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--operand-sets", type=int, default=None,

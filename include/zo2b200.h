@@ -133,6 +133,20 @@ typedef struct zo2_segment_desc {
  * per SM (the engine sets 1 when K2 runs on the prepare stream concurrently
  * with the GEMMs, operand_sets = 2). */
 int zo2_set_k2_ctas_per_sm(int n);
+/* K2 variant (process-wide).  0 (default): codec arenas (bf16 / f16 / e4m3
+ * wire) with bf16 or no operands take the certified path -- binary32 chain on
+ * an approximate z with a verified error bound, each output kept only when
+ * its rounding is provably the exact chain's, else recomputed with the exact
+ * z; bit-identical results.  1: always the queued exact kernel (A/B). */
+int zo2_set_k2_variant(int variant);
+/* Exhaustive check of the approximate z's bound (zo2_zapprox.cuh) over every
+ * binary32 y in [2^-24, 1/2]; writes 32 floats to d_out (device): [0] max
+ * |z~ - z| / tau, [1] max |z~ - z|, [2] mapping mismatches, [3 + b] max
+ * |z~ - z| / (1 + |z~|) per binade of y.  Test support. */
+int zo2_zapprox_bound_probe(float *d_out, void *cuda_stream);
+/* Elements the certified K2 path recomputed with the exact z since the last
+ * reset (synchronous read of a device counter; diagnostics and tests). */
+int zo2_k2c_fallbacks(uint64_t *out, int reset);
 int zo2_update_perturb(void *arena, int wire_fmt, uint64_t n, uint64_t base,
                        int update, const double *d_g, double lr,
                        uint64_t lrs_seed, int perturb, double eps,

@@ -58,6 +58,9 @@ _SIGS = {
                                    POINTER(SegmentDesc), c_int, c_void_p, c_void_p]),
     "zo2_set_k2_ctas_per_sm": (c_int, [c_int]),
     "zo2_set_rng_mode": (c_int, [c_int]),
+    "zo2_set_k2_variant": (c_int, [c_int]),
+    "zo2_zapprox_bound_probe": (c_int, [c_void_p, c_void_p]),
+    "zo2_k2c_fallbacks": (c_int, [POINTER(c_uint64), c_int]),
     "zo2_host_register": (c_int, [c_void_p, c_uint64]),
     "zo2_host_unregister": (c_int, [c_void_p]),
     "zo2_rng_mode": (c_int, []),

@@ -31,6 +31,7 @@
 #include "zo2_wire.cuh"
 #include "zo2_zexact.cuh"
 #include "zo2_rng_fast.h"
+#include "zo2_zapprox.cuh"
 #include <string.h>
 
 void zo2_count_launch(uint64_t n = 1);
@@ -65,6 +66,7 @@ struct K2Table {
   uint32_t tiles_c[MAX_SEGS];   // column tiles (transposed segments)
   uint8_t transposed[MAX_SEGS];
   int n;
+  int any_transposed;
 };
 
 struct K2Params {
@@ -242,8 +244,10 @@ __device__ __forceinline__ void k2_tiles(void *arena, const K2Table &T, const K2
     uint64_t e0 = 0, idx;
     int cnt, widx;
     if (tr) {
-      r0 = (uint32_t)(ltile / T.tiles_c[si]) * 32;
-      c0 = (uint32_t)(ltile % T.tiles_c[si]) * 32;
+      // 32-bit division: a segment has < 2^32 tiles
+      const uint32_t lt = (uint32_t)ltile, tc = T.tiles_c[si], q = lt / tc;
+      r0 = q * 32;
+      c0 = (lt - q * tc) * 32;
       const uint32_t r = r0 + (t >> 3), c = c0 + 4 * (t & 7);
       cnt = (r < sg.rows && c < sg.cols) ? (int)min(4u, sg.cols - c) : 0;
       idx = sg.offset + (uint64_t)r * sg.cols + c;
@@ -502,6 +506,488 @@ __global__ void __launch_bounds__(NT, ZO2_K2_MINB) k_update_perturb(void *arena,
   if (FMT != ZO2_F32 && FMT != ZO2_F64) add_counts(counts, nn, ns);
 }
 
+// ============================================================================
+// K2c: the certified path for codec arenas (bf16 / f16 / e4m3 wire) whose
+// matrix operands are bf16 -- the AMP configurations 3-5.  Every output of
+// the element chain is a narrow rounding (arena code, bf16 operand), so the
+// chain runs in binary32 on z~ (zo2_zapprox.cuh) and an output is kept only
+// if the whole interval [v - M, v + M] that provably contains the exact
+// chain's value encodes to one code (the encoders are monotone).  Elements
+// that fail (~1e-3 at the model's weight scales) are appended to a per-stream
+// fix-up list and recomputed with the exact z (Philox4x64 + Cephes in IEEE
+// double, axpy1 NaN rules) by a second kernel on the same stream, 32 per
+// warp, so the rare exact element costs a lane, not a diverged warp.  The
+// result is the reference's bits either way.  Vector segments (f32 operands
+// for LN / bias epilogues) always take the exact chain inline.
+//
+// Error bound.  Exact chain (chain_exact): x = f32(w + f64(uc zu));
+// ez = f64(eps zp); p = f32(x + ez); m = f32(p - 2 ez); w' = f32(m + ez).
+// Here: x~ = fma32(uc, z~u, w), e = f32(eps z~p), p~ = f32(x~ + e),
+// m~ = fma32(-2, e, p~), w~' = f32(m~ + e).  With Du = x~ - x - r0 and
+// D = e - ez (the same D enters all three steps, it is one number):
+//   p~ - p  = (x~ - x) + D + r1
+//   m~ - m  = (p~ - p) - 2D + r2 = (x~ - x) - D + r1 + r2
+//   w~' - w' = (m~ - m) + D + r3 = (x~ - x) + r1 + r2 + r3
+// |ri| <= 2^-24 |vi| (round to nearest), |x~ - x| <= |uc| tau_u + 2^-24
+// (|uc z~u| + 2|x|), |D| <= eps tau_p + 2^-23 |e|; the f64 roundings of the
+// exact chain are 2^-29 of these.  So with A = max |x|, |p|, |m|, |w'|:
+//   M_pm = |uc| tau_u + eps tau_p + 2^-22 (A + |uc z~u| + |e|)
+//   M_w  = |uc| tau_u + 2^-22 (A + |uc z~u|)        (z~p cancels in w')
+// (times 1.01), so the restored arena weight almost never needs the exact z.
+// ============================================================================
+constexpr int TP = 33;  // transposed staging pitch (u32 words)
+// elements recomputed with the exact z (diagnostics: zo2_k2c_fallbacks)
+__device__ unsigned long long g_k2c_redo = 0;
+
+struct K2cEntry {
+  uint64_t idx;  // element index in the module bucket
+  float w0;      // decoded arena value before the chain
+  uint32_t pad;
+};
+struct K2cList {
+  unsigned long long *count;  // device counter, zeroed before every K2c launch
+  unsigned long long cap;
+  K2cEntry *e;
+};
+
+// the codec's code of a finite value below cert_lim (no NaN / saturation
+// cases): bf16 RNE on the bits (numerics.py:232-245), f16 cvt.rn (numpy's
+// cast), e4m3 the full encoder
+template <int FMT>
+__device__ __forceinline__ uint32_t code_of(float v) {
+  if (FMT == ZO2_BF16) {
+    const uint32_t u = __float_as_uint(v);
+    return (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+  }
+  if (FMT == ZO2_F16) return __half_as_ushort(__float2half_rn(v));
+  unsigned a = 0, b = 0;
+  return enc_e4m3(v, a, b);
+}
+template <int FMT>
+__device__ __forceinline__ void store1_cert(void *arena, uint64_t i, float w) {
+  if (FMT == ZO2_F8E4M3) ((uint8_t *)arena)[i] = (uint8_t)code_of<FMT>(w);
+  else ((uint16_t *)arena)[i] = (uint16_t)code_of<FMT>(w);
+}
+// store 4 certified values (codes as code_of), or fall back to the codec
+template <int FMT>
+__device__ __forceinline__ void store4_cert(void *arena, uint64_t i, const float w[4], unsigned &nn,
+                                            unsigned &ns) {
+  if (FMT == ZO2_BF16) {
+    uint2 v;
+    v.x = code_of<FMT>(w[0]) | (code_of<FMT>(w[1]) << 16);
+    v.y = code_of<FMT>(w[2]) | (code_of<FMT>(w[3]) << 16);
+    *(uint2 *)((uint16_t *)arena + i) = v;
+  } else if (FMT == ZO2_F16) {
+    uint2 v;
+    v.x = code_of<FMT>(w[0]) | (code_of<FMT>(w[1]) << 16);
+    v.y = code_of<FMT>(w[2]) | (code_of<FMT>(w[3]) << 16);
+    *(uint2 *)((uint16_t *)arena + i) = v;
+  } else {
+    Wire<FMT>::store4(arena, i, w, nn, ns);
+  }
+}
+// below these magnitudes no value of the interval saturates (so the codec's
+// saturation counter cannot differ between the two chains)
+template <int FMT> __device__ __forceinline__ float cert_lim() {
+  return FMT == ZO2_BF16 ? 1e38f : FMT == ZO2_F16 ? 32768.0f : 256.0f;
+}
+
+__device__ __forceinline__ uint64_t raw_at(const ZxKeys &K, uint64_t pos) {
+  uint64_t b[4];
+  zx_philox_block_k(K, pos >> 2, b);
+  const unsigned l = (unsigned)(pos & 3);
+  return l == 0 ? b[0] : l == 1 ? b[1] : l == 2 ? b[2] : b[3];
+}
+
+// the exact element: Philox4x64 + Cephes (zo2_rng.h) + axpy1 chain
+template <bool UPD, bool PERT>
+__device__ __noinline__ Chain3<float> cert_exact(float w, const ZxKeys2 &KS, uint64_t pos,
+                                                  double uc, double eps) {
+  const double zu = UPD ? zo2_ndtri(zo2_u53(raw_at(KS.lrs, pos))) : 0.0;
+  const double zp = PERT ? zo2_ndtri(zo2_u53(raw_at(KS.rs, pos))) : 0.0;
+  return chain_exact<UPD, PERT, float>(w, uc, zu, eps, zp);
+}
+
+// z~ for the 4 draws of one Philox block, warp-converged: Giles' central
+// polynomial for every draw, the tail one only when some lane needs it
+// (same operations as za_g, so the same values the bound probe checked).
+__device__ __forceinline__ void za_z4(const uint64_t r[4], float z[4], float tau[4]) {
+  float w[4], x[4];
+  bool up[4], tail = false;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float y = za_y(r[j], up[j]);
+    x[j] = __fmaf_rn(-2.0f, y, 1.0f);
+    const float a = __fmul_rn(__fmul_rn(4.0f, y), __fsub_rn(1.0f, y));
+    w[j] = __fmul_rn(za_lg2(a), -0.69314718056f);
+    tau[j] = y >= ZA_Y_MIN ? 0.0f : __int_as_float(0x7f800000);
+    tail |= !(w[j] < 5.0f);
+  }
+  float p[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) p[j] = za_central(__fsub_rn(w[j], 2.5f));
+  if (__any_sync(0xffffffffu, tail)) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (!(w[j] < 5.0f)) p[j] = za_tailp(__fsub_rn(za_sqrt(w[j]), 3.0f));
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float g = __fmul_rn(1.41421356237f, __fmul_rn(p[j], x[j]));
+    tau[j] = __fadd_rn(tau[j], __fmaf_rn(ZA_TAU_REL, g, ZA_TAU_ABS));
+    z[j] = up[j] ? g : -g;
+  }
+}
+
+template <int FMT, bool UPD, bool PERT>
+__device__ void k2c_exact_inline(void *arena, uint64_t idx, float w0, const ZxKeys2 &KS,
+                                 const K2Params &P, float &w, float &op, float &om) {
+  const Chain3<float> c = cert_exact<UPD, PERT>(w0, KS, P.base + idx, P.ucoef, P.eps);
+  w = c.w;
+  op = c.wp;
+  om = c.wm;
+}
+
+template <int FMT, bool UPD, bool PERT>
+__device__ __forceinline__ void k2c_tiles(void *arena, const K2Table &T, const K2Params &P,
+                                          const ZxKeys2 &KS, K2cList L, uint32_t (*S)[32 * TP],
+                                          unsigned &nn, unsigned &ns) {
+  const int t = threadIdx.x;
+  const float ucf = (float)P.ucoef, epsf = (float)P.eps;
+  const float auc = fabsf(ucf), aeps = fabsf(epsf);
+  const uint64_t total = T.tile_start[T.n];
+  int buf = 0, si = 0;
+  for (uint64_t tile = blockIdx.x; tile < total; tile += gridDim.x, buf ^= 1) {
+    while (tile >= T.tile_start[si + 1]) ++si;
+    const zo2_segment_desc &sg = T.s[si];
+    const bool tr = T.transposed[si] != 0;
+    const uint64_t ltile = tile - T.tile_start[si];
+    uint32_t r0 = 0, c0 = 0;
+    uint64_t e0 = 0, idx;
+    int cnt;
+    if (tr) {
+      // 32-bit division: a segment has < 2^32 tiles
+      const uint32_t lt = (uint32_t)ltile, tc = T.tiles_c[si], q = lt / tc;
+      r0 = q * 32;
+      c0 = (lt - q * tc) * 32;
+      const uint32_t r = r0 + (t >> 3), c = c0 + 4 * (t & 7);
+      cnt = (r < sg.rows && c < sg.cols) ? (int)min(4u, sg.cols - c) : 0;
+      idx = sg.offset + (uint64_t)r * sg.cols + c;
+    } else {
+      e0 = ltile * TE;
+      const uint64_t seg_n = (uint64_t)sg.rows * sg.cols;
+      const uint64_t e = e0 + 4 * (uint64_t)t;
+      cnt = e < seg_n ? (int)min((uint64_t)4, seg_n - e) : 0;
+      idx = sg.offset + e;
+    }
+    const int kind = PERT ? sg.out_kind : ZO2_OUT_NONE;
+    float w[4] = {0.f, 0.f, 0.f, 0.f}, op[4], om[4];
+    const bool vec = cnt == 4 && (idx & 3) == 0;
+    if (vec) Wire<FMT>::load4(arena, idx, w);
+    else
+      for (int j = 0; j < cnt; ++j) w[j] = Wire<FMT>::load1(arena, idx + j);
+    unsigned inl = 0;  // elements computed by the exact chain here (codec-encoded)
+    if (kind == ZO2_OUT_F32) {
+      inl = (1u << cnt) - 1u;
+      // vector segment (tile-uniform): f32 operands need the exact chain
+      for (int j = 0; j < cnt; ++j)
+        k2c_exact_inline<FMT, UPD, PERT>(arena, idx + j, w[j], KS, P, w[j], op[j], om[j]);
+    } else {
+      // the warp stays converged here (lanes past a segment edge compute
+      // unused values): za_z4 votes across the warp
+      float zu[4], tu[4], zp[4], tp[4];
+      uint64_t r[4];
+      if (UPD) {
+        zx_raw4_k(KS.lrs, P.base + idx, r);
+        za_z4(r, zu, tu);
+      }
+      if (PERT) {
+        zx_raw4_k(KS.rs, P.base + idx, r);
+        za_z4(r, zp, tp);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float x0 = w[j];
+        float x = x0, e = 0.f, p, m, wn;
+        float Mu = 0.f, R = 0.f;
+        if (UPD) {
+          x = __fmaf_rn(ucf, zu[j], x0);
+          Mu = __fmul_rn(auc, tu[j]);
+          R = __fmul_rn(auc, fabsf(zu[j]));
+        }
+        if (PERT) {
+          e = __fmul_rn(epsf, zp[j]);
+          p = __fadd_rn(x, e);
+          m = __fmaf_rn(-2.0f, e, p);
+          wn = __fadd_rn(m, e);
+        } else {
+          p = m = wn = x;
+        }
+        const float A = fmaxf(fmaxf(fabsf(x0), fabsf(x)), fmaxf(fabsf(p), fabsf(m)));
+        // R: magnitudes the roundings scale with (+ eps tau_p, so that an
+        // unusable z~p, tau = inf, also voids the arena check)
+        float Mp = Mu;
+        R = __fadd_rn(R, A);
+        if (PERT) {
+          const float et = __fmul_rn(aeps, tp[j]);
+          R = __fadd_rn(R, __fadd_rn(fabsf(e), et));
+          Mp = __fadd_rn(Mp, et);
+        }
+        const float Mw = __fmul_rn(__fmaf_rn(0x1p-22f, R, Mu), 1.01f);
+        bool ok = (A < cert_lim<FMT>()) && (Mw < 1e30f) &&
+                  code_of<FMT>(__fsub_rd(wn, Mw)) == code_of<FMT>(__fadd_ru(wn, Mw));
+        if (kind != ZO2_OUT_NONE) {
+          Mp = __fmul_rn(__fmaf_rn(0x1p-22f, R, Mp), 1.01f);
+          ok = ok && bf16x2(__fsub_rd(p, Mp), __fsub_rd(m, Mp)) ==
+                         bf16x2(__fadd_ru(p, Mp), __fadd_ru(m, Mp));
+        }
+        op[j] = p;
+        om[j] = m;
+        w[j] = wn;
+        if (!ok && j < cnt) {
+          const unsigned long long slot = atomicAdd(L.count, 1ull);
+          atomicAdd(&g_k2c_redo, 1ull);
+          if (slot < L.cap) {
+            L.e[slot].idx = idx + j;
+            L.e[slot].w0 = x0;
+            w[j] = 0.0f;  // placeholder code (no codec counts); fix-up rewrites it
+          } else {       // list full: this element inline
+            k2c_exact_inline<FMT, UPD, PERT>(arena, idx + j, x0, KS, P, w[j], op[j], om[j]);
+            inl |= 1u << j;
+          }
+        }
+      }
+    }
+    // restored (updated) weights, re-encoded, straight back to the arena;
+    // exact-chain elements (NaN / saturation possible) through the codec
+    if (vec && !inl) store4_cert<FMT>(arena, idx, w, nn, ns);
+    else
+      for (int j = 0; j < cnt; ++j) {
+        if ((inl >> j) & 1u) Wire<FMT>::store1(arena, idx + j, w[j], nn, ns);
+        else store1_cert<FMT>(arena, idx + j, w[j]);
+      }
+    if (kind == ZO2_OUT_F32 && cnt > 0) {
+      const uint64_t o = e0 + 4 * (uint64_t)t;
+      for (int j = 0; j < cnt; ++j) {
+        ((float *)sg.out_plus)[o + j] = op[j];
+        ((float *)sg.out_minus)[o + j] = om[j];
+      }
+    } else if (kind == ZO2_OUT_BF16 && cnt > 0) {
+      const uint64_t o = e0 + 4 * (uint64_t)t;
+      if (vec) {
+        *(uint2 *)((__nv_bfloat16 *)sg.out_plus + o) = make_uint2(bf16x2(op[0], op[1]), bf16x2(op[2], op[3]));
+        *(uint2 *)((__nv_bfloat16 *)sg.out_minus + o) = make_uint2(bf16x2(om[0], om[1]), bf16x2(om[2], om[3]));
+      } else {
+        for (int j = 0; j < cnt; ++j) {
+          ((__nv_bfloat16 *)sg.out_plus)[o + j] = __float2bfloat16_rn(op[j]);
+          ((__nv_bfloat16 *)sg.out_minus)[o + j] = __float2bfloat16_rn(om[j]);
+        }
+      }
+    } else if (kind == ZO2_OUT_BF16_T) {
+      // stage (p | m << 16) bf16 pairs [r][c], write operand rows [c][r]
+      uint32_t *St = S[buf];
+      const int sb = (t >> 3) * TP + 4 * (t & 7);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) St[sb + j] = bf16x2(op[j], om[j]);
+      __syncthreads();
+      const int c = t >> 3, rb = 4 * (t & 7);
+      if (c0 + c < sg.cols && r0 + rb < sg.rows) {
+        const int acnt = (int)min(4u, sg.rows - (r0 + rb));
+        uint32_t v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = St[(rb + i) * TP + c];
+        const uint64_t o = (uint64_t)(c0 + c) * sg.rows + r0 + rb;
+        if (acnt == 4 && (o & 3) == 0) {
+          *(uint2 *)((uint16_t *)sg.out_plus + o) =
+              make_uint2((v[0] & 0xFFFFu) | (v[1] << 16), (v[2] & 0xFFFFu) | (v[3] << 16));
+          *(uint2 *)((uint16_t *)sg.out_minus + o) =
+              make_uint2((v[0] >> 16) | (v[1] & 0xFFFF0000u), (v[2] >> 16) | (v[3] & 0xFFFF0000u));
+        } else {
+          for (int i = 0; i < acnt; ++i) {
+            ((uint16_t *)sg.out_plus)[o + i] = (uint16_t)(v[i] & 0xFFFFu);
+            ((uint16_t *)sg.out_minus)[o + i] = (uint16_t)(v[i] >> 16);
+          }
+        }
+      }
+    }
+    if (kind != ZO2_OUT_BF16_T && T.any_transposed) {
+      // one barrier in every tile: S[buf] is rewritten two tiles later, after
+      // the next tile's barrier, whatever kind that tile is
+      __syncthreads();
+    }
+  }
+}
+
+#ifndef ZO2_K2C_MINB
+#define ZO2_K2C_MINB 3
+#endif
+template <int FMT>
+__global__ void __launch_bounds__(NT, ZO2_K2C_MINB) k_update_perturb_cert(void *arena, K2Table T, K2Params P,
+                                                            const __grid_constant__ ZxKeys2 KS,
+                                                            const double *d_g, double lr,
+                                                            uint64_t *counts, K2cList L) {
+  __shared__ uint32_t S[2][32 * TP];
+  int upd = P.do_update;
+  P.ucoef = resolve_ucoef(d_g, lr, upd);
+  unsigned nn = 0, ns = 0;
+  if (upd && P.do_perturb) k2c_tiles<FMT, true, true>(arena, T, P, KS, L, S, nn, ns);
+  else if (upd) k2c_tiles<FMT, true, false>(arena, T, P, KS, L, S, nn, ns);
+  else if (P.do_perturb) k2c_tiles<FMT, false, true>(arena, T, P, KS, L, S, nn, ns);
+  else k2c_tiles<FMT, false, false>(arena, T, P, KS, L, S, nn, ns);
+  add_counts(counts, nn, ns);
+}
+
+// Fix-up of the listed elements (stream-ordered after k_update_perturb_cert):
+// exact chain, arena code and operands rewritten at their positions.
+template <int FMT>
+__global__ void __launch_bounds__(128) k_k2c_fixup(void *arena, K2Table T, K2Params P,
+                                                   const __grid_constant__ ZxKeys2 KS,
+                                                   const double *d_g, double lr,
+                                                   uint64_t *counts, K2cList L) {
+  int upd = P.do_update;
+  P.ucoef = resolve_ucoef(d_g, lr, upd);
+  const uint64_t n = min(*L.count, L.cap);
+  unsigned nn = 0, ns = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const K2cEntry en = L.e[i];
+    Chain3<float> c;
+    if (upd && P.do_perturb) c = cert_exact<true, true>(en.w0, KS, P.base + en.idx, P.ucoef, P.eps);
+    else if (upd) c = cert_exact<true, false>(en.w0, KS, P.base + en.idx, P.ucoef, P.eps);
+    else if (P.do_perturb) c = cert_exact<false, true>(en.w0, KS, P.base + en.idx, P.ucoef, P.eps);
+    else c = cert_exact<false, false>(en.w0, KS, P.base + en.idx, P.ucoef, P.eps);
+    Wire<FMT>::store1(arena, en.idx, c.w, nn, ns);
+    if (!P.do_perturb) continue;
+    int k = 0;
+    while (k + 1 < T.n && en.idx >= T.s[k + 1].offset) ++k;
+    const zo2_segment_desc &sg = T.s[k];
+    const uint64_t rel = en.idx - sg.offset;
+    uint64_t o = rel;
+    if (T.transposed[k]) o = (rel % sg.cols) * sg.rows + rel / sg.cols;
+    if (sg.out_kind == ZO2_OUT_BF16 || sg.out_kind == ZO2_OUT_BF16_T) {
+      ((__nv_bfloat16 *)sg.out_plus)[o] = __float2bfloat16_rn(c.wp);
+      ((__nv_bfloat16 *)sg.out_minus)[o] = __float2bfloat16_rn(c.wm);
+    }
+  }
+  // all lanes reach this point (no early return): warp-collective counts
+  add_counts(counts, nn, ns);
+}
+
+// 0 = certified path where it applies (default), 1 = always the queued exact kernel
+int g_k2_variant = 0;
+
+// fix-up lists, one per CUDA stream (K2c launches on one stream are ordered)
+struct K2cSlot {
+  cudaStream_t s;
+  void *buf;
+  unsigned long long cap;
+};
+K2cSlot g_k2c_slots[16];
+int g_k2c_nslots = 0;
+
+int k2c_list_for(cudaStream_t s, uint64_t n, K2cList &L) {
+  const unsigned long long want = n >> 9 > (1ull << 18) ? n >> 9 : (1ull << 18);
+  K2cSlot *sl = nullptr;
+  for (int i = 0; i < g_k2c_nslots; ++i)
+    if (g_k2c_slots[i].s == s) sl = &g_k2c_slots[i];
+  if (!sl) {
+    if (g_k2c_nslots == 16) sl = &g_k2c_slots[15];  // recycle (synchronised below)
+    else sl = &g_k2c_slots[g_k2c_nslots++];
+    sl->s = s;
+    sl->buf = nullptr;
+    sl->cap = 0;
+  }
+  if (sl->cap < want) {
+    if (sl->buf) {
+      ZO2_CUDA_TRY(cudaDeviceSynchronize());
+      ZO2_CUDA_TRY(cudaFree(sl->buf));
+    }
+    ZO2_CUDA_TRY(cudaMalloc(&sl->buf, 16 + want * sizeof(K2cEntry)));
+    sl->cap = want;
+  }
+  L.count = (unsigned long long *)sl->buf;
+  L.cap = sl->cap;
+  L.e = (K2cEntry *)((char *)sl->buf + 16);
+  return ZO2_OK;
+}
+
+template <int FMT>
+int launch_k2c(void *arena, const K2Table &T, const K2Params &P, const double *d_g, double lr,
+               uint64_t *counts, cudaStream_t s) {
+  const uint64_t tiles = T.tile_start[T.n];
+  if (tiles == 0) return ZO2_OK;
+  static int occ = 0;
+  if (occ == 0) {
+    ZO2_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_perturb_cert<FMT>, NT, 0));
+    if (occ < 1) occ = 1;
+  }
+  unsigned per_sm = (unsigned)occ;
+  if (g_k2_ctas_per_sm && g_k2_ctas_per_sm < per_sm) per_sm = g_k2_ctas_per_sm;
+  const uint64_t cap = 148ull * per_sm;
+  const unsigned g = (unsigned)(tiles < cap ? tiles : cap);
+  ZxKeys2 KS;
+  zx_round_keys(P.lrs_seed, ZO2_PERTURB_STREAM, KS.lrs);
+  zx_round_keys(P.rs_seed, ZO2_PERTURB_STREAM, KS.rs);
+  K2cList L;
+  const int rc = k2c_list_for(s, tiles * TE, L);
+  if (rc != ZO2_OK) return rc;
+  ZO2_CUDA_TRY(cudaMemsetAsync(L.count, 0, sizeof(unsigned long long), s));
+  k_update_perturb_cert<FMT><<<g, NT, 0, s>>>(arena, T, P, KS, d_g, lr, counts, L);
+  zo2_count_launch();
+  ZO2_CHECK_LAUNCH();
+  k_k2c_fixup<FMT><<<148, 128, 0, s>>>(arena, T, P, KS, d_g, lr, counts, L);
+  zo2_count_launch();
+  ZO2_CHECK_LAUNCH();
+  return ZO2_OK;
+}
+
+// ---------------------------------------------------------------- bound probe
+// For every binary32 y in [2^-24, 1/2]: the 53-bit integers y53 whose
+// fl32((2 y53 + 1) 2^-54) is y form one interval; z is monotone in the raw
+// integer, so the exact z at the interval ends (both sides of 1/2) bracket
+// every exact z that shares this z~.  out[0] = max |z~ - z| / tau(z~),
+// out[1] = max |z~ - z|, out[2] = za_y mismatches at the ends (must be 0),
+// out[3 + b] = max |z~ - z| / (1 + |z~|) in binade b of y (2^(b-24)).
+__device__ __forceinline__ void atomic_max_pos(float *a, float v) {
+  atomicMax((int *)a, __float_as_int(v));
+}
+__global__ void k_zapprox_probe(float *out) {
+  const uint32_t lo = 0x33800000u, hi = 0x3F000000u;  // 2^-24 .. 0.5
+  float mr = 0.f, ma = 0.f, mismatch = 0.f;
+  for (uint32_t b = lo + blockIdx.x * blockDim.x + threadIdx.x; b <= hi;
+       b += gridDim.x * blockDim.x) {
+    const float f = __uint_as_float(b);
+    const float fu = __uint_as_float(b + 1), fd = __uint_as_float(b - 1);
+    const uint64_t F = (uint64_t)((double)f * 0x1p54);
+    const uint64_t hu = (uint64_t)(((double)fu - (double)f) * 0x1p53);
+    const uint64_t hd = (uint64_t)(((double)f - (double)fd) * 0x1p53);
+    uint64_t nlo = F - hd + 1, nhi = F + hu - 1;
+    if (nhi > (1ull << 53) - 1) nhi = (1ull << 53) - 1;
+    const float g = za_g(f);
+    const float tau = __fmaf_rn(ZA_TAU_REL, g, ZA_TAU_ABS);
+    float mrel = 0.f;
+    for (int end = 0; end < 2; ++end) {
+      const uint64_t y53 = ((end ? nhi : nlo) - 1) >> 1;
+      for (int side = 0; side < 2; ++side) {
+        const uint64_t m = side ? ((1ull << 53) - 1 - y53) : y53;
+        bool upper;
+        if (za_y(m << 11, upper) != f || upper != (side != 0)) mismatch += 1.f;
+        const double z = zo2_ndtri(zo2_u53(m << 11));
+        const float za = side ? g : -g;
+        const float err = (float)fabs((double)za - z);
+        mr = fmaxf(mr, err / tau);
+        ma = fmaxf(ma, err);
+        mrel = fmaxf(mrel, err / (1.f + g));
+      }
+    }
+    const int bin = (int)((b >> 23) & 0xFF) - (127 - 24);
+    atomic_max_pos(&out[3 + bin], mrel);
+  }
+  atomic_max_pos(&out[0], mr);
+  atomic_max_pos(&out[1], ma);
+  if (mismatch > 0.f) atomicAdd(&out[2], mismatch);
+}
+
 template <int FMT, bool FAST>
 int launch_k2(void *arena, const K2Table &T, const K2Params &P, const double *d_g, double lr,
               uint64_t *counts, cudaStream_t s) {
@@ -534,6 +1020,33 @@ int launch_k2(void *arena, const K2Table &T, const K2Params &P, const double *d_
 extern "C" int zo2_set_k2_ctas_per_sm(int n) {
   if (n < 0 || n > 32) return zo2_set_error(ZO2_E_ARG, "zo2_set_k2_ctas_per_sm: 0..32");
   g_k2_ctas_per_sm = (unsigned)n;
+  return ZO2_OK;
+}
+
+extern "C" int zo2_set_k2_variant(int v) {
+  if (v != 0 && v != 1) return zo2_set_error(ZO2_E_ARG, "zo2_set_k2_variant: 0 (certified where valid) or 1 (queued exact)");
+  g_k2_variant = v;
+  return ZO2_OK;
+}
+
+extern "C" int zo2_k2c_fallbacks(uint64_t *out, int reset) {
+  if (!out) return zo2_set_error(ZO2_E_ARG, "zo2_k2c_fallbacks: null output");
+  unsigned long long v = 0;
+  ZO2_CUDA_TRY(cudaMemcpyFromSymbol(&v, g_k2c_redo, sizeof(v)));
+  *out = v;
+  if (reset) {
+    v = 0;
+    ZO2_CUDA_TRY(cudaMemcpyToSymbol(g_k2c_redo, &v, sizeof(v)));
+  }
+  return ZO2_OK;
+}
+
+extern "C" int zo2_zapprox_bound_probe(float *d_out, void *cs) {
+  if (!d_out) return zo2_set_error(ZO2_E_ARG, "zo2_zapprox_bound_probe: null output");
+  ZO2_CUDA_TRY(cudaMemsetAsync(d_out, 0, 32 * sizeof(float), (cudaStream_t)cs));
+  k_zapprox_probe<<<148 * 8, 256, 0, (cudaStream_t)cs>>>(d_out);
+  zo2_count_launch();
+  ZO2_CHECK_LAUNCH();
   return ZO2_OK;
 }
 
@@ -572,6 +1085,7 @@ extern "C" int zo2_update_perturb(void *arena, int wire_fmt, uint64_t n, uint64_
     T.s[k] = sg;
     if (!perturb) T.s[k].out_kind = ZO2_OUT_NONE;
     T.transposed[k] = (t && perturb) ? 1 : 0;
+    T.any_transposed |= T.transposed[k];
     uint64_t tiles;
     if (T.transposed[k]) {
       T.tiles_c[k] = (sg.cols + 31) / 32;
@@ -593,6 +1107,20 @@ extern "C" int zo2_update_perturb(void *arena, int wire_fmt, uint64_t n, uint64_
   P.rs_seed = rs_seed;
   cudaStream_t s = (cudaStream_t)cs;
   const bool fast = g_rng_mode == 1;
+  bool cert = !fast && g_k2_variant == 0 &&
+              (wire_fmt == ZO2_BF16 || wire_fmt == ZO2_F16 || wire_fmt == ZO2_F8E4M3);
+  for (int k = 0; k < n_segs && cert; ++k) {
+    const int kd = T.s[k].out_kind;
+    cert = kd == ZO2_OUT_NONE || kd == ZO2_OUT_BF16 || kd == ZO2_OUT_BF16_T ||
+           (kd == ZO2_OUT_F32 && !T.transposed[k]);
+  }
+  if (cert) {
+    switch (wire_fmt) {
+      case ZO2_BF16: return launch_k2c<ZO2_BF16>(arena, T, P, d_g, lr, counts, s);
+      case ZO2_F16: return launch_k2c<ZO2_F16>(arena, T, P, d_g, lr, counts, s);
+      default: return launch_k2c<ZO2_F8E4M3>(arena, T, P, d_g, lr, counts, s);
+    }
+  }
   switch (wire_fmt) {
     case ZO2_F64: return fast ? launch_k2<ZO2_F64, true>(arena, T, P, d_g, lr, counts, s)
                           : launch_k2<ZO2_F64, false>(arena, T, P, d_g, lr, counts, s);

@@ -275,6 +275,69 @@ def test_update_perturb_full_size_codec_block(cuda, dim, codec):
     assert torch.equal(op.hi.view(-1), wq.view(-1).to(torch.bfloat16))
 
 
+# ------------------------------------------------------------------ K2c
+def test_zapprox_bound_exhaustive(cuda):
+    """The certified K2 path's error bound tau(z~) (zo2_zapprox.cuh) holds for
+    EVERY binary32 y in [2^-24, 1/2]: exact z at both ends of each y's integer
+    interval, both sides of 1/2, within tau/4 (a 4x safety factor)."""
+    _l = L()
+    out = torch.zeros(32, dtype=torch.float32, device=cuda)
+    _l.call("zo2_zapprox_bound_probe", out.data_ptr(), stream())
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    print("zapprox: max err/tau", o[0], "max abs err", o[1], "per-binade", o[3:27].tolist())
+    assert o[2] == 0, "za_y maps an interval end to another float"
+    assert 0 < o[0] <= 0.5, o[0]
+
+
+def _scaled_weights(n, seed):
+    g = np.random.default_rng(seed)
+    w = g.standard_normal(n) * 10.0 ** g.uniform(-9, 1, n)
+    return w.astype(np.float32)
+
+
+@pytest.mark.parametrize("codec", ["bf16", "f16", "f8"])
+@pytest.mark.parametrize("lr,g", [(1e-7, 2.5), (1e-3, -1.0), (0.0, 0.0)])
+def test_k2_certified_equals_queued_exact(cuda, codec, lr, g):
+    """K2c (certified binary32 chain + exact fallback) against the queued exact
+    kernel on the same codec arena and bf16 operands (transposed and linear
+    segments), with weights spread over ten decades so both the common path
+    and the fallback run: arena codes, operands and codec counters identical."""
+    from paper_2503_12668_b200.model import DualForward, ModelSpec, module_size
+    _l = L()
+    spec = ModelSpec(1, 256, 2, 512, 64)
+    n = module_size(spec, "block.0")
+    w = _scaled_weights(n, 7)
+    w[:6] = [np.nan, 1e5, -1e5, 0.0, -0.0, 3e-39]
+    from oracle import zo2_oracle as O
+    fmt = {"bf16": _l.BF16, "f16": _l.F16, "f8": _l.F8E4M3}[codec]
+    bits, _, _ = O.encode(w, codec)
+    src = torch.from_numpy(bits.view(np.int16) if bits.dtype == np.uint16 else bits).to(cuda)
+    res = []
+    for variant in (1, 0):
+        _l.call("zo2_set_k2_variant", variant)
+        fwd = DualForward(spec, 1, "bf16", cuda, 1)
+        arena = src.clone()
+        d_g = torch.tensor([g], dtype=torch.float64, device=cuda)
+        counts = torch.zeros(2, dtype=torch.int64, device=cuda)
+        descs = fwd.block_descs(0)
+        _l.call("zo2_update_perturb", arena.data_ptr(), fmt, n, 5_000_003, 1 if lr else 0,
+                d_g.data_ptr(), lr, 0x77, 1, 1e-3, 0x99, descs, len(descs), counts.data_ptr(),
+                stream())
+        torch.cuda.synchronize()
+        vec, mat = fwd.sets[0]
+        ops = {k: (v[0].hi.clone(), v[1].hi.clone()) for k, v in mat.items()}
+        ops.update({k: (v[0].clone(), v[1].clone()) for k, v in vec.items()})
+        res.append((arena.view(torch.uint8).clone(), ops, counts.cpu().tolist()))
+    _l.call("zo2_set_k2_variant", 0)
+    (a1, o1, c1), (a0, o0, c0) = res
+    assert torch.equal(a1, a0), int((a1 != a0).sum())
+    assert c1 == c0
+    for k in o1:
+        for x, y in zip(o1[k], o0[k]):
+            assert torch.equal(x.view(torch.uint8), y.view(torch.uint8)), k
+
+
 # ------------------------------------------------------------------ K9
 @pytest.mark.parametrize("fmt", ["bf16", "f16", "f8"])
 def test_codecs_bit_exact(cuda, golden, fmt):

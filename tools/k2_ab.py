@@ -1,6 +1,7 @@
 """A/B timing of K2 (tools only): ZO2_LIB_PATH selects the library, ZO2_RNG
 the z generator; K2_ARENA=f32|bf16 and K2_DIM set the arena format (bf16 =
 codec arena with bf16 operands, the AMP configurations) and the width."""
+import ctypes
 import os
 import sys
 
@@ -11,16 +12,18 @@ from paper_2503_12668_b200 import _lib  # noqa: E402
 from paper_2503_12668_b200.model import DualForward, ModelSpec, module_size  # noqa: E402
 
 _lib.call("zo2_set_rng_mode", 1 if os.environ.get("ZO2_RNG") == "fast" else 0)
+_lib.call("zo2_set_k2_variant", int(os.environ.get("K2_VARIANT", "0")))
 arena_fmt = os.environ.get("K2_ARENA", "f32")
 dim = int(os.environ.get("K2_DIM", "2048"))
-spec = ModelSpec(1, dim, dim // 64, 50272, 512)
+spec = ModelSpec(1, dim, dim // 128 if dim >= 4096 else dim // 64, 50272, 512)
 fwd = DualForward(spec, 1, "f32" if arena_fmt == "f32" else "bf16", "cuda", 1)
 n = module_size(spec, "block.0")
 w = torch.randn(n, device="cuda") * 0.02
 if arena_fmt == "f32":
     arena, code = w, _lib.F32
 else:
-    arena, code = w.to(torch.bfloat16).view(torch.int16), _lib.BF16
+    tdt = torch.float16 if arena_fmt == "f16" else torch.bfloat16
+    arena, code = w.to(tdt).view(torch.int16), (_lib.F16 if arena_fmt == "f16" else _lib.BF16)
 d_g = torch.tensor([1.5], dtype=torch.float64, device="cuda")
 counts = torch.zeros(2, dtype=torch.int64, device="cuda")
 descs = fwd.block_descs(0)
@@ -43,5 +46,8 @@ for _ in range(R):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / R
-print(f"{_lib.LIB_PATH.split('/')[-1]} rng={os.environ.get('ZO2_RNG', 'exact')} arena={arena_fmt} "
+fb = ctypes.c_uint64(0)
+_lib.call("zo2_k2c_fallbacks", ctypes.byref(fb), 1)
+print(f"fallbacks per run {fb.value / (R + 3):.0f} of {n} ({fb.value / (R + 3) / n:.2e}) ", end="")
+print(f"variant={os.environ.get('K2_VARIANT', '0')} rng={os.environ.get('ZO2_RNG', 'exact')} arena={arena_fmt} "
       f"d={dim} K2 block ms {ms:.3f}  Gz/s {2 * n / ms / 1e6:.1f}")
