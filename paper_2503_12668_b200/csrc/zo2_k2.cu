@@ -67,6 +67,9 @@ struct K2Table {
   uint8_t transposed[MAX_SEGS];
   int n;
   int any_transposed;
+  // K2c warp tiles: 32 rows x 4 columns (transposed) or 128 linear elements
+  uint64_t wt_start[MAX_SEGS + 1];
+  uint32_t wt_c[MAX_SEGS];      // 4-column groups per row band (transposed)
 };
 
 struct K2Params {
@@ -535,7 +538,6 @@ __global__ void __launch_bounds__(NT, ZO2_K2_MINB) k_update_perturb(void *arena,
 //   M_w  = |uc| tau_u + 2^-22 (A + |uc z~u|)        (z~p cancels in w')
 // (times 1.01), so the restored arena weight almost never needs the exact z.
 // ============================================================================
-constexpr int TP = 33;  // transposed staging pitch (u32 words)
 // elements recomputed with the exact z (diagnostics: zo2_k2c_fallbacks)
 __device__ unsigned long long g_k2c_redo = 0;
 
@@ -648,48 +650,73 @@ __device__ void k2c_exact_inline(void *arena, uint64_t idx, float w0, const ZxKe
   om = c.wm;
 }
 
+// Coordinates of warp tile `wt`: lane = row (transposed: 32 rows x 4 columns,
+// the lane's 4 elements are one Philox block of its row) or 4 consecutive
+// elements (linear: 128 per warp).  Operand rows [N, K] of a transposed
+// segment are then written as 32 consecutive bf16 per column: coalesced,
+// without a shared-memory transpose or a barrier.
+struct K2cTile {
+  uint64_t idx, o;  // first element in the bucket; first operand index
+  int si, cnt, ostride;
+};
+__device__ __forceinline__ void k2c_coords(const K2Table &T, uint64_t wt, int &si, int lane,
+                                           K2cTile &c) {
+  while (wt >= T.wt_start[si + 1]) ++si;  // tiles ascend: si never moves back
+  const zo2_segment_desc &sg = T.s[si];
+  const uint64_t lt = wt - T.wt_start[si];
+  c.si = si;
+  if (T.transposed[si]) {
+    const uint32_t l = (uint32_t)lt, q = l / T.wt_c[si];
+    const uint32_t r = q * 32 + lane, col = (l - q * T.wt_c[si]) * 4;
+    c.cnt = (r < sg.rows) ? (int)min(4u, sg.cols - col) : 0;
+    c.idx = sg.offset + (uint64_t)r * sg.cols + col;
+    c.o = (uint64_t)col * sg.rows + r;  // operand [cols][rows]
+    c.ostride = (int)sg.rows;
+  } else {
+    const uint64_t seg_n = (uint64_t)sg.rows * sg.cols;
+    const uint64_t e = lt * 128 + 4 * (uint64_t)lane;
+    c.cnt = e < seg_n ? (int)min((uint64_t)4, seg_n - e) : 0;
+    c.idx = sg.offset + e;
+    c.o = e;
+    c.ostride = 1;
+  }
+}
+
+template <int FMT>
+__device__ __forceinline__ void k2c_load(const void *arena, const K2cTile &c, float w[4]) {
+  w[0] = w[1] = w[2] = w[3] = 0.f;
+  if (c.cnt == 4 && (c.idx & 3) == 0) Wire<FMT>::load4(arena, c.idx, w);
+  else
+    for (int j = 0; j < c.cnt; ++j) w[j] = Wire<FMT>::load1(arena, c.idx + j);
+}
+
 template <int FMT, bool UPD, bool PERT>
 __device__ __forceinline__ void k2c_tiles(void *arena, const K2Table &T, const K2Params &P,
-                                          const ZxKeys2 &KS, K2cList L, uint32_t (*S)[32 * TP],
-                                          unsigned &nn, unsigned &ns) {
-  const int t = threadIdx.x;
+                                          const ZxKeys2 &KS, K2cList L, unsigned &nn,
+                                          unsigned &ns) {
+  const int lane = threadIdx.x & 31;
   const float ucf = (float)P.ucoef, epsf = (float)P.eps;
   const float auc = fabsf(ucf), aeps = fabsf(epsf);
-  const uint64_t total = T.tile_start[T.n];
-  int buf = 0, si = 0;
-  for (uint64_t tile = blockIdx.x; tile < total; tile += gridDim.x, buf ^= 1) {
-    while (tile >= T.tile_start[si + 1]) ++si;
-    const zo2_segment_desc &sg = T.s[si];
-    const bool tr = T.transposed[si] != 0;
-    const uint64_t ltile = tile - T.tile_start[si];
-    uint32_t r0 = 0, c0 = 0;
-    uint64_t e0 = 0, idx;
-    int cnt;
-    if (tr) {
-      // 32-bit division: a segment has < 2^32 tiles
-      const uint32_t lt = (uint32_t)ltile, tc = T.tiles_c[si], q = lt / tc;
-      r0 = q * 32;
-      c0 = (lt - q * tc) * 32;
-      const uint32_t r = r0 + (t >> 3), c = c0 + 4 * (t & 7);
-      cnt = (r < sg.rows && c < sg.cols) ? (int)min(4u, sg.cols - c) : 0;
-      idx = sg.offset + (uint64_t)r * sg.cols + c;
-    } else {
-      e0 = ltile * TE;
-      const uint64_t seg_n = (uint64_t)sg.rows * sg.cols;
-      const uint64_t e = e0 + 4 * (uint64_t)t;
-      cnt = e < seg_n ? (int)min((uint64_t)4, seg_n - e) : 0;
-      idx = sg.offset + e;
-    }
+  const uint64_t total = T.wt_start[T.n];
+  const uint64_t stride = (uint64_t)gridDim.x * (NT / 32);
+  uint64_t wt = (uint64_t)blockIdx.x * (NT / 32) + (threadIdx.x >> 5);
+  int si = 0;
+  K2cTile cur;
+  for (; wt < total; wt += stride) {
+    // (prefetching the next tile's weights here measured 5% slower: spills)
+    k2c_coords(T, wt, si, lane, cur);
+    float w[4], op[4], om[4];
+    k2c_load<FMT>(arena, cur, w);
+    const K2cTile c = cur;
+    const zo2_segment_desc &sg = T.s[c.si];
     const int kind = PERT ? sg.out_kind : ZO2_OUT_NONE;
-    float w[4] = {0.f, 0.f, 0.f, 0.f}, op[4], om[4];
+    const int cnt = c.cnt;
+    const uint64_t idx = c.idx;
     const bool vec = cnt == 4 && (idx & 3) == 0;
-    if (vec) Wire<FMT>::load4(arena, idx, w);
-    else
-      for (int j = 0; j < cnt; ++j) w[j] = Wire<FMT>::load1(arena, idx + j);
     unsigned inl = 0;  // elements computed by the exact chain here (codec-encoded)
     if (kind == ZO2_OUT_F32) {
-      inl = (1u << cnt) - 1u;
-      // vector segment (tile-uniform): f32 operands need the exact chain
+      // vector segment (warp-uniform): f32 operands need the exact chain
+      inl = cnt > 0 ? (1u << cnt) - 1u : 0u;
       for (int j = 0; j < cnt; ++j)
         k2c_exact_inline<FMT, UPD, PERT>(arena, idx + j, w[j], KS, P, w[j], op[j], om[j]);
     } else {
@@ -766,54 +793,41 @@ __device__ __forceinline__ void k2c_tiles(void *arena, const K2Table &T, const K
         if ((inl >> j) & 1u) Wire<FMT>::store1(arena, idx + j, w[j], nn, ns);
         else store1_cert<FMT>(arena, idx + j, w[j]);
       }
-    if (kind == ZO2_OUT_F32 && cnt > 0) {
-      const uint64_t o = e0 + 4 * (uint64_t)t;
+    if (kind == ZO2_OUT_F32) {
       for (int j = 0; j < cnt; ++j) {
-        ((float *)sg.out_plus)[o + j] = op[j];
-        ((float *)sg.out_minus)[o + j] = om[j];
+        ((float *)sg.out_plus)[c.o + j] = op[j];
+        ((float *)sg.out_minus)[c.o + j] = om[j];
       }
-    } else if (kind == ZO2_OUT_BF16 && cnt > 0) {
-      const uint64_t o = e0 + 4 * (uint64_t)t;
+    } else if (kind == ZO2_OUT_BF16) {
       if (vec) {
-        *(uint2 *)((__nv_bfloat16 *)sg.out_plus + o) = make_uint2(bf16x2(op[0], op[1]), bf16x2(op[2], op[3]));
-        *(uint2 *)((__nv_bfloat16 *)sg.out_minus + o) = make_uint2(bf16x2(om[0], om[1]), bf16x2(om[2], om[3]));
+        *(uint2 *)((__nv_bfloat16 *)sg.out_plus + c.o) = make_uint2(bf16x2(op[0], op[1]), bf16x2(op[2], op[3]));
+        *(uint2 *)((__nv_bfloat16 *)sg.out_minus + c.o) = make_uint2(bf16x2(om[0], om[1]), bf16x2(om[2], om[3]));
       } else {
         for (int j = 0; j < cnt; ++j) {
-          ((__nv_bfloat16 *)sg.out_plus)[o + j] = __float2bfloat16_rn(op[j]);
-          ((__nv_bfloat16 *)sg.out_minus)[o + j] = __float2bfloat16_rn(om[j]);
+          ((__nv_bfloat16 *)sg.out_plus)[c.o + j] = __float2bfloat16_rn(op[j]);
+          ((__nv_bfloat16 *)sg.out_minus)[c.o + j] = __float2bfloat16_rn(om[j]);
         }
       }
     } else if (kind == ZO2_OUT_BF16_T) {
-      // stage (p | m << 16) bf16 pairs [r][c], write operand rows [c][r]
-      uint32_t *St = S[buf];
-      const int sb = (t >> 3) * TP + 4 * (t & 7);
+      // column j of the tile -> operand row (col + j), this lane's K position:
+      // 32 lanes write 32 consecutive bf16 (64 B) per column and sign
+      const uint32_t pp01 = bf16x2(op[0], op[1]), pp23 = bf16x2(op[2], op[3]);
+      const uint32_t mm01 = bf16x2(om[0], om[1]), mm23 = bf16x2(om[2], om[3]);
+      const uint32_t pv[2] = {pp01, pp23}, mv[2] = {mm01, mm23};
+      uint16_t *P_ = (uint16_t *)sg.out_plus + c.o, *M_ = (uint16_t *)sg.out_minus + c.o;
+      const uint64_t os = (uint64_t)c.ostride;
+      if (cnt == 4) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) St[sb + j] = bf16x2(op[j], om[j]);
-      __syncthreads();
-      const int c = t >> 3, rb = 4 * (t & 7);
-      if (c0 + c < sg.cols && r0 + rb < sg.rows) {
-        const int acnt = (int)min(4u, sg.rows - (r0 + rb));
-        uint32_t v[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] = St[(rb + i) * TP + c];
-        const uint64_t o = (uint64_t)(c0 + c) * sg.rows + r0 + rb;
-        if (acnt == 4 && (o & 3) == 0) {
-          *(uint2 *)((uint16_t *)sg.out_plus + o) =
-              make_uint2((v[0] & 0xFFFFu) | (v[1] << 16), (v[2] & 0xFFFFu) | (v[3] << 16));
-          *(uint2 *)((uint16_t *)sg.out_minus + o) =
-              make_uint2((v[0] >> 16) | (v[1] & 0xFFFF0000u), (v[2] >> 16) | (v[3] & 0xFFFF0000u));
-        } else {
-          for (int i = 0; i < acnt; ++i) {
-            ((uint16_t *)sg.out_plus)[o + i] = (uint16_t)(v[i] & 0xFFFFu);
-            ((uint16_t *)sg.out_minus)[o + i] = (uint16_t)(v[i] >> 16);
-          }
+        for (int j = 0; j < 4; ++j) {
+          P_[j * os] = (uint16_t)(pv[j >> 1] >> (16 * (j & 1)));
+          M_[j * os] = (uint16_t)(mv[j >> 1] >> (16 * (j & 1)));
+        }
+      } else {
+        for (int j = 0; j < cnt; ++j) {
+          P_[j * os] = (uint16_t)(pv[j >> 1] >> (16 * (j & 1)));
+          M_[j * os] = (uint16_t)(mv[j >> 1] >> (16 * (j & 1)));
         }
       }
-    }
-    if (kind != ZO2_OUT_BF16_T && T.any_transposed) {
-      // one barrier in every tile: S[buf] is rewritten two tiles later, after
-      // the next tile's barrier, whatever kind that tile is
-      __syncthreads();
     }
   }
 }
@@ -826,14 +840,13 @@ __global__ void __launch_bounds__(NT, ZO2_K2C_MINB) k_update_perturb_cert(void *
                                                             const __grid_constant__ ZxKeys2 KS,
                                                             const double *d_g, double lr,
                                                             uint64_t *counts, K2cList L) {
-  __shared__ uint32_t S[2][32 * TP];
   int upd = P.do_update;
   P.ucoef = resolve_ucoef(d_g, lr, upd);
   unsigned nn = 0, ns = 0;
-  if (upd && P.do_perturb) k2c_tiles<FMT, true, true>(arena, T, P, KS, L, S, nn, ns);
-  else if (upd) k2c_tiles<FMT, true, false>(arena, T, P, KS, L, S, nn, ns);
-  else if (P.do_perturb) k2c_tiles<FMT, false, true>(arena, T, P, KS, L, S, nn, ns);
-  else k2c_tiles<FMT, false, false>(arena, T, P, KS, L, S, nn, ns);
+  if (upd && P.do_perturb) k2c_tiles<FMT, true, true>(arena, T, P, KS, L, nn, ns);
+  else if (upd) k2c_tiles<FMT, true, false>(arena, T, P, KS, L, nn, ns);
+  else if (P.do_perturb) k2c_tiles<FMT, false, true>(arena, T, P, KS, L, nn, ns);
+  else k2c_tiles<FMT, false, false>(arena, T, P, KS, L, nn, ns);
   add_counts(counts, nn, ns);
 }
 
@@ -914,7 +927,7 @@ int k2c_list_for(cudaStream_t s, uint64_t n, K2cList &L) {
 template <int FMT>
 int launch_k2c(void *arena, const K2Table &T, const K2Params &P, const double *d_g, double lr,
                uint64_t *counts, cudaStream_t s) {
-  const uint64_t tiles = T.tile_start[T.n];
+  const uint64_t tiles = (T.wt_start[T.n] + NT / 32 - 1) / (NT / 32);  // CTA-sized groups
   if (tiles == 0) return ZO2_OK;
   static int occ = 0;
   if (occ == 0) {
@@ -929,7 +942,7 @@ int launch_k2c(void *arena, const K2Table &T, const K2Params &P, const double *d
   zx_round_keys(P.lrs_seed, ZO2_PERTURB_STREAM, KS.lrs);
   zx_round_keys(P.rs_seed, ZO2_PERTURB_STREAM, KS.rs);
   K2cList L;
-  const int rc = k2c_list_for(s, tiles * TE, L);
+  const int rc = k2c_list_for(s, T.wt_start[T.n] * 128, L);
   if (rc != ZO2_OK) return rc;
   ZO2_CUDA_TRY(cudaMemsetAsync(L.count, 0, sizeof(unsigned long long), s));
   k_update_perturb_cert<FMT><<<g, NT, 0, s>>>(arena, T, P, KS, d_g, lr, counts, L);
@@ -1094,6 +1107,14 @@ extern "C" int zo2_update_perturb(void *arena, int wire_fmt, uint64_t n, uint64_
       tiles = (sn + TE - 1) / TE;
     }
     T.tile_start[k + 1] = T.tile_start[k] + tiles;
+    uint64_t wt;
+    if (T.transposed[k]) {
+      T.wt_c[k] = (sg.cols + 3) / 4;
+      wt = (uint64_t)((sg.rows + 31) / 32) * T.wt_c[k];
+    } else {
+      wt = (sn + 127) / 128;
+    }
+    T.wt_start[k + 1] = T.wt_start[k] + wt;
   }
   T.n = n_segs;
   if (covered != n) return zo2_set_error(ZO2_E_ARG, "zo2_update_perturb: segments do not cover n");
