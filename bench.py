@@ -149,51 +149,73 @@ class Clocks:
 # CPU baseline: the reference's step (oracle port), bounded sample
 # ----------------------------------------------------------------------------
 _CPU_STATE: dict = {}
+CPU_SUB_BATCH = 1
 
 
-def cpu_step_sample(spec_t, B, lr):
-    """Time the oracle's deferred ZO2 step pieces on this host and scale them to
-    one full step: per block = RNG passes (update + 3 perturb passes over 1/8
-    of the block, x32) + dual forward at batch 2 (x B/2); embed + head
-    likewise.  Returns (seconds per full step, sample description)."""
+def _cpu_setup(cfg):
+    """Reduced-depth reference model at FULL width (1 block, the embedding and
+    the head) for the CPU arm.  Setup, not timed: random weights (values do not
+    change the work), the wire codec applied once like the reference's
+    construction-time encode."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
     from oracle import zo2_oracle as O
-    nb, d, H, V, S = spec_t
-    spec = O.Spec(1, d, H, V, S)
-    key = (spec_t, B)
-    if key not in _CPU_STATE:  # setup (init + data) is not part of the sample
-        _CPU_STATE[key] = (O.init_params(spec, SEED), O.gen_synthetic(V, S, 4, SEED))
-    p, (tok, tgt) = _CPU_STATE[key]
-    bsub = 2
-    scale = B / bsub
-    tk, tg = tok[:bsub], tgt[:bsub]
-    blk = p["block.0"]
-    part = blk[: blk.size // 8].copy()
+    key = cfg["workload"]
+    if key not in _CPU_STATE:
+        nb, d, H, V, S = cfg["spec"]
+        spec = O.Spec(1, d, H, V, S)
+        pool = ThreadPoolExecutor(os.cpu_count() or 1)
+        rng = np.random.default_rng(SEED)
+        p = {}
+        for m, lay in O.layouts(spec).items():
+            n = sum(int(np.prod(sh)) for _, sh in lay)
+            p[m] = (rng.standard_normal(n, dtype=np.float32) * np.float32(0.02))
+        tok, tgt = O.gen_synthetic(V, S, 4, SEED)
+        _CPU_STATE[key] = (spec, p, tok[:CPU_SUB_BATCH], tgt[:CPU_SUB_BATCH], pool)
+    return _CPU_STATE[key]
+
+
+def cpu_reference_step(cfg, j):
+    """ONE WHOLE reference ZO2 step (oracle port of zo2lab's deferred step,
+    zo2_engine.py:183-204 / :264-316) on this host: embedding, one full-width
+    block, head; the deferred update and +eps/-2eps/+eps RNG passes over every
+    parameter (all host threads), the wire codec round trip of the block
+    (upload decode + offload encode), dual forward at batch CPU_SUB_BATCH x S,
+    f64 cross-entropy.  Returns (seconds of the whole reduced step, estimate of
+    the full step, breakdown): the full step is extrapolated EXPLICITLY as
+    embed + head + n_blocks x block, with the forward phases scaled by
+    B / CPU_SUB_BATCH (RNG and codec work do not depend on the batch)."""
+    from oracle import zo2_oracle as O
+    spec, p, tok, tgt, pool = _cpu_setup(cfg)
+    key = ("eng", cfg["workload"])
+    if key not in _CPU_STATE:
+        codec = cfg["codec"] if cfg["codec"] != "none" else None
+        _CPU_STATE[key] = O.Zo2Sequential(spec, p, EPS, cfg["lr"], SEED, pool=pool, codec=codec)
+    eng = _CPU_STATE[key]
+    eng.t = {}
     t0 = time.perf_counter()
-    for c in (-(lr * 1.0), EPS, -2 * EPS, EPS):
-        O.axpy_z(part, c, 12345, 0)
-    t_rng_block = (time.perf_counter() - t0) * 8
-    h = O.fwd_embed(spec, p["embed"], tk)
-    t0 = time.perf_counter()
-    for _ in range(2):
-        O.fwd_block(spec, blk, h)
-    t_fwd_block = (time.perf_counter() - t0) * scale
-    t0 = time.perf_counter()
-    for _ in range(2):
-        O.fwd_embed(spec, p["embed"], tk)
-    t_embed = (time.perf_counter() - t0) * scale
-    headw = p["head"].reshape(V, d)
-    t0 = time.perf_counter()
-    for _ in range(2):
-        O.ce_loss(h @ headw.T, tg)
-    t_head = (time.perf_counter() - t0) * scale
-    n_res = p["embed"].size + p["head"].size
-    t_rng_res = t_rng_block * n_res / blk.size
-    total = nb * (t_rng_block + t_fwd_block) + t_rng_res + t_embed + t_head
-    desc = (f"oracle ZO2 step pieces on host: 1 block RNG passes on 1/8 of the block (x32), "
-            f"1 block dual forward at batch {bsub}x{S} (x{scale:g}), embed+head dual forward "
-            f"at batch {bsub} (x{scale:g}), resident-module RNG scaled by size; "
-            f"estimate = {nb} x block + embed + head")
-    return total, desc
+    eng.step(tok, tgt, j)
+    measured = time.perf_counter() - t0
+    nb, B = cfg["spec"][0], cfg["B"]
+    scale = B / CPU_SUB_BATCH
+    parts = {}
+    for kind in ("embed", "block", "head"):
+        rng_s = eng.t.get((kind, "rng"), 0.0) + eng.t.get((kind, "codec"), 0.0)
+        fwd_s = eng.t.get((kind, "fwd"), 0.0)
+        parts[kind] = {"rng_codec_s": rng_s, "fwd_s": fwd_s,
+                       "full_s": rng_s + fwd_s * scale}
+    full = parts["embed"]["full_s"] + parts["head"]["full_s"] + nb * parts["block"]["full_s"]
+    return measured, full, parts
+
+
+def cpu_sample_desc(cfg):
+    nb, d, H, V, S = cfg["spec"]
+    return (f"oracle port of the reference ZO2 step, {os.cpu_count()} host threads: each "
+            f"timed step is one WHOLE step of a reduced-depth model at full width (embedding "
+            f"{V}+{S}x{d}, 1 of {nb} blocks, head {V}x{d}; deferred update + 3 perturb passes "
+            f"over all parameters, block wire codec '{cfg['codec']}', dual forward at batch "
+            f"{CPU_SUB_BATCH}x{S}, f64 CE); value = {cfg['B']}x{S} tokens / (embed + head + "
+            f"{nb} x block), forward phases x{cfg['B'] // CPU_SUB_BATCH} for batch {cfg['B']}")
 
 
 def link_probe(dev, nbytes=1 << 30, reps=3):
@@ -248,42 +270,47 @@ def full_depth_estimate(tls, cfg, tokens_step):
             "step_ms": step * 1e3, "tokens_per_s": tokens_step / step}
 
 
-def cpu_threads():
-    try:
-        from threadpoolctl import threadpool_info
-        th = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
-    except Exception:
-        th = os.cpu_count() or 1
-    return int(th)
-
-
 def run_reference(args, cfg, rank, world):
-    """--impl reference: the reference's CPU path on this host (rank 0 only)."""
+    """--impl reference: the reference's CPU path on this host (rank 0 only),
+    whole reduced-depth steps with an explicit full-depth extrapolation."""
     if rank != 0:
         return
-    nb, d, H, V, S = cfg["spec"]
+    S = cfg["spec"][4]
     tokens = cfg["B"] * S
-    for _ in range(args.warmup):
-        cpu_step_sample(cfg["spec"], cfg["B"], cfg["lr"])
-    ts = []
-    desc = ""
-    for _ in range(args.steps):
-        t, desc = cpu_step_sample(cfg["spec"], cfg["B"], cfg["lr"])
-        ts.append(t)
-    step_s = statistics.median(ts)
+    for j in range(args.warmup):
+        cpu_reference_step(cfg, j)
+    meas, full, parts = [], [], None
+    for k in range(args.steps):
+        m, f, parts = cpu_reference_step(cfg, args.warmup + k)
+        meas.append(m)
+        full.append(f)
+    step_s = statistics.median(full)
     value = tokens / step_s
     line = {"impl": "reference", "metric": "ZO step tokens/s", "value": value,
             "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "global_batch": cfg["B"], "seq_len": S,
-                       "model": "reference toy block at OPT geometry (random init)",
-                       "parallelism": "cpu"},
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_threads(),
-                             "kind": "port", "sample": desc},
+            "config": config_dict(cfg, world),
+            "arm": {"impl": "oracle port of zo2lab (numpy + C restatement), CPU",
+                    "compute": "f32 forward (numpy BLAS), f64 CE, reference z stream"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": os.cpu_count(),
+                             "kind": "port", "sample": cpu_sample_desc(cfg)},
+            "extrapolation": {"measured_reduced_step_s": meas,
+                              "full_step_s": full, "per_module_last_step": parts,
+                              "formula": "embed + head + n_blocks x block, forward x B/sub_batch"},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def config_dict(cfg, world):
+    """The workload description both arms print (identical dicts)."""
+    nb, d, H, V, S = cfg["spec"]
+    return {"workload": cfg["workload"], "model": f"OPT geometry {nb}x{d}, {H} heads, V={V}",
+            "global_batch": cfg["B"] * world, "seq_len": S,
+            "parallelism": f"dp{world}" if world > 1 else "single",
+            "wire": cfg["codec"] if cfg["codec"] != "none" else "f32",
+            "l2": "inputs larger than L2 (GBs of weights streamed per step)"}
 
 
 # ----------------------------------------------------------------------------
@@ -494,22 +521,20 @@ def run_ours(args, cfg, rank, world, local_rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16x3" if split else "bf16", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "model": f"OPT geometry {nb}x{d}, V={V}",
-                   "global_batch": B * world, "seq_len": S,
-                   "parallelism": (f"dp{world}" + (" (shared masters, sharded PCIe + NVLink "
-                                                   "all-gather)" if sharded else "")
-                                   if world > 1 else "single"),
-                   "wire": cfg["codec"] if cfg["codec"] != "none" else "f32",
-                   "compute": ("f32 parameters / update / LN / CE; GEMMs as bf16x3 splits "
-                               "(hi*hi + hi*lo + lo*hi, ~16-bit operand mantissas, f32 "
-                               "accumulate)" if split else
-                               "bf16 GEMM operands, f32 accumulate; f32 parameters / update / "
-                               "LN / softmax / residual, CE in f64"),
-                   "l2": "inputs larger than L2 (4.8+ GB of weights streamed per step)",
-                   "rng": args.rng + (" (reference z stream, bit-exact)" if args.rng == "exact"
-                                      else " (Philox4x32 + binary32 erfinv, not the reference's z)"),
-                   "steps_pipelined": not args.no_pipeline,
-                   "operand_sets": eng.operand_sets},
+        "config": config_dict(cfg, world),
+        "arm": {"parallelism_detail": ("shared host masters, sharded PCIe + NVLink all-gather"
+                                       if sharded else ("replicated host masters"
+                                                        if world > 1 else None)),
+                "compute": ("f32 parameters / update / LN / CE; GEMMs as bf16x3 splits "
+                            "(hi*hi + hi*lo + lo*hi, ~16-bit operand mantissas, f32 "
+                            "accumulate)" if split else
+                            "bf16 compute (bf16 GEMM operands, f32 accumulate; f32 "
+                            "parameters / update / LN / softmax / residual, CE in f64), "
+                            f"{cfg['codec']} wire"),
+                "rng": args.rng + (" (reference z stream, bit-exact)" if args.rng == "exact"
+                                   else " (Philox4x32 + binary32 erfinv, not the reference's z)"),
+                "steps_pipelined": not args.no_pipeline,
+                "operand_sets": eng.operand_sets},
         "roofline": {"bound": "tensor", "kernel": "zo2_gemm (tcgen05 cta_group::2, fused epilogues)",
                      "achieved": gemm_tflops, "peak": peak_bf16 / passes,
                      "unit": "TFLOP/s", "frac": (gemm_tflops * passes / peak_bf16
@@ -559,14 +584,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         "losses_tail": eng.losses[-2:],
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ts = []
-        desc = ""
-        for _ in range(3):
-            t, desc = cpu_step_sample(cfg["spec"], B, cfg["lr"])
-            ts.append(t)
-        cs = statistics.median(ts)
-        line["cpu_baseline"] = {"value": T / cs, "unit": "tokens/s", "cores": cpu_threads(),
-                                "kind": "port", "sample": desc}
+        cpu_reference_step(cfg, 0)  # first call: setup + numpy/BLAS warm-up
+        meas, full, _ = cpu_reference_step(cfg, 1)
+        line["cpu_baseline"] = {"value": T / full, "unit": "tokens/s", "cores": os.cpu_count(),
+                                "kind": "port", "sample": cpu_sample_desc(cfg),
+                                "measured_reduced_step_s": meas, "full_step_s": full}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if shm is not None:

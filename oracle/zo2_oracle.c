@@ -171,6 +171,18 @@ void oracle_gaussian_fill(uint64_t seed, uint64_t stream, uint64_t counter,
   }
 }
 
+/* z at arbitrary stream positions counter + idx[i] (sampled checks of
+ * whole-block kernels; same Philox block + lane + ndtri as the fill). */
+void oracle_gauss_at(uint64_t seed, uint64_t stream, uint64_t counter,
+                     const uint64_t *idx, uint64_t n, double *out) {
+  uint64_t buf[4];
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t pos = counter + idx[i];
+    philox_at_block(pos >> 2, seed, stream, buf);
+    out[i] = oracle_ndtri(u53(buf[pos & 3]));
+  }
+}
+
 uint64_t oracle_derive_step_seed(uint64_t base, uint64_t j) {
   uint64_t x = base ^ (j * 0x9E3779B97F4A7C15ULL);
   x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;

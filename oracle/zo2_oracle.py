@@ -48,6 +48,7 @@ def lib():
         vp = ctypes.c_void_p
         L.oracle_raw_u64.argtypes = [U64, U64, U64, U64, vp]
         L.oracle_gaussian_fill.argtypes = [U64, U64, U64, U64, vp]
+        L.oracle_gauss_at.argtypes = [U64, U64, U64, vp, U64, vp]
         L.oracle_derive_step_seed.argtypes = [U64, U64]
         L.oracle_derive_step_seed.restype = U64
         L.oracle_axpy_z_f32.argtypes = [vp, U64, ctypes.c_double, U64, U64, U64]
@@ -164,6 +165,23 @@ def axpy_z_fast(flat: np.ndarray, coef: float, seed: int, counter: int) -> None:
         return
     z = fast_gauss(seed, PERTURB, counter, flat.size).astype(np.float64)
     flat[:] = (flat.astype(np.float64) + np.float64(coef) * z).astype(flat.dtype)
+
+
+def gauss_at(seed: int, stream: int, counter: int, idx: np.ndarray) -> np.ndarray:
+    """z(seed, stream, counter + idx[i]) for arbitrary positions (numerics.py:161-168)."""
+    idx = np.ascontiguousarray(idx, np.uint64)
+    out = np.empty(idx.size, np.float64)
+    lib().oracle_gauss_at(seed & M64, stream & M64, counter & M64, idx.ctypes.data, idx.size,
+                          out.ctypes.data)
+    return out
+
+
+def axpy_z_at(vals: np.ndarray, idx: np.ndarray, coef: float, seed: int,
+              counter: int) -> np.ndarray:
+    """vals[i] + coef * z(seed, PERTURB, counter + idx[i]) with axpy_z's single
+    rounding (f64 product and sum, store in vals' dtype; model.py:227-233)."""
+    z = gauss_at(seed, PERTURB, counter, idx)
+    return (vals.astype(np.float64) + np.float64(coef) * z).astype(vals.dtype)
 
 
 def derive_step_seed(base: int, j: int) -> int:
@@ -370,25 +388,74 @@ class MeZO:
         return g
 
 
+def axpy_z_threaded(flat: np.ndarray, coef: float, seed: int, counter: int, pool) -> None:
+    """axpy_z over disjoint chunks in a thread pool (ctypes releases the GIL):
+    z positions are absolute (numerics.py:161-168), so the bytes equal one call."""
+    n, step = flat.size, 1 << 22
+    list(pool.map(lambda o: axpy_z(flat[o:o + step], coef, seed, counter + o),
+                  range(0, n, step)))
+
+
+def codec_roundtrip_threaded(flat: np.ndarray, fmt: str, pool) -> None:
+    """The reference's offload encode + upload decode of one block master
+    (runtime.py:145-199), chunk-parallel: flat <- decode(encode(flat))."""
+    step = 1 << 22
+
+    def job(o):
+        flat[o:o + step] = decode(encode(flat[o:o + step], fmt)[0], fmt)
+    list(pool.map(job, range(0, flat.size, step)))
+
+
 class Zo2Sequential:
     """The deferred per-module ZO2 step (zo2_engine.py:183-204, :264-336),
-    executed module by module on the CPU; used as the timed CPU baseline."""
+    executed module by module on the CPU; used as the timed CPU baseline.
 
-    def __init__(self, spec, params, eps, lr, seed):
+    pool: optional thread pool for the RNG passes and the wire codec; codec:
+    the AMP wire format of transferable blocks (upload decode + offload encode
+    per block per step); self.t accumulates seconds per (module kind, phase)
+    for the bench's explicit full-depth extrapolation."""
+
+    def __init__(self, spec, params, eps, lr, seed, pool=None, codec=None):
         self.spec, self.p, self.eps, self.lr, self.seed = spec, params, eps, lr, seed
         self.off = offsets(spec)
         self.pending_g, self.lrs_seed = 0.0, None
         self.losses, self.gs = [], []
+        self.pool, self.codec = pool, codec
+        self.t: dict = {}
+
+    def _axpy(self, flat, coef, seed, ctr):
+        if self.pool is None:
+            axpy_z(flat, coef, seed, ctr)
+        else:
+            axpy_z_threaded(flat, coef, seed, ctr, self.pool)
+
+    def _tick(self, m, phase, t0):
+        import time
+        kind = "block" if m.startswith("block.") else m
+        now = time.perf_counter()
+        self.t[(kind, phase)] = self.t.get((kind, phase), 0.0) + now - t0
+        return now
 
     def _module(self, m, x_plus, x_minus, s):
+        import time
         flat = self.p[m]
+        t0 = time.perf_counter()
+        block = m.startswith("block.")
+        if block and self.codec:
+            codec_roundtrip_threaded(flat, self.codec, self.pool)  # upload + last offload
+            t0 = self._tick(m, "codec", t0)
         if self.pending_g != 0.0 and flat.size:
-            axpy_z(flat, -(self.lr * self.pending_g), self.lrs_seed, self.off[m])
-        axpy_z(flat, self.eps, s, self.off[m])
+            self._axpy(flat, -(self.lr * self.pending_g), self.lrs_seed, self.off[m])
+        self._axpy(flat, self.eps, s, self.off[m])
+        t0 = self._tick(m, "rng", t0)
         op = self._fwd(m, x_plus)
-        axpy_z(flat, -2.0 * self.eps, s, self.off[m])
+        t0 = self._tick(m, "fwd", t0)
+        self._axpy(flat, -2.0 * self.eps, s, self.off[m])
+        t0 = self._tick(m, "rng", t0)
         om = self._fwd(m, x_minus)
-        axpy_z(flat, self.eps, s, self.off[m])
+        t0 = self._tick(m, "fwd", t0)
+        self._axpy(flat, self.eps, s, self.off[m])
+        self._tick(m, "rng", t0)
         return op, om
 
     def _fwd(self, m, x):
@@ -403,7 +470,10 @@ class Zo2Sequential:
         xp, xm = tokens, tokens
         for m in self.p:
             xp, xm = self._module(m, xp, xm, s)
+        import time
+        t0 = time.perf_counter()
         lp, lm = ce_loss(xp, targets), ce_loss(xm, targets)
+        self._tick("head", "fwd", t0)
         g = (lp - lm) / (2.0 * self.eps)
         self.pending_g, self.lrs_seed = g, s
         self.losses.append(lp)

@@ -35,6 +35,9 @@ from .scheduler import (CudaLanes, Lane, build_iteration_dag, build_prepare_dag,
                         validate_timeline)
 
 
+# markers for update coefficients resolved when the iteration's g is known
+_G_PREV, _G_CUR = object(), object()
+
 # z generator per engine (zo2b200.h zo2_set_rng_mode): "exact" is the
 # reference's stream (numerics.py:161-182), "fast" the GPU-cost Philox4x32
 # direction; the mode is process-wide in the library and set before every
@@ -205,8 +208,12 @@ class _DeviceStep:
             raise ValueError(f"tokens shape {tokens.shape} invalid for seq_len {self.spec.seq_len}")
         if tokens.shape[1] != self.spec.seq_len:
             raise ValueError("the B200 forward requires full-length sequences (S == seq_len)")
-        if tokens.min() < 0 or tokens.max() >= self.spec.vocab:
+        if tokens.size and (tokens.min() < 0 or tokens.max() >= self.spec.vocab):
             raise ValueError("token id out of range")
+        # the CE epilogue only records a target logit for 0 <= target < vocab:
+        # refuse instead of silently forming a wrong loss (and a wrong g)
+        if targets.size and (targets.min() < 0 or targets.max() >= self.spec.vocab):
+            raise ValueError(f"target id out of range [0, {self.spec.vocab})")
         fwd = self.ensure(tokens.shape[0])
         i = self.h_tok_i = (self.h_tok_i + 1) % len(self.h_tok_ring)
         if self.h_tok_ev[i] is not None:
@@ -267,7 +274,8 @@ class Zo2Engine:
         self.lanes = CudaLanes(runtime.device)
         self.dev = _DeviceStep(workload.spec, workload.arith, runtime.device, self.operand_sets)
         self._set_k2_grid()
-        self._pool_booked = False
+        self._booked: dict[str, int] = {}  # DevicePool booking of self.dev.fwd
+        self._booked_fwd = None
         self._async: list = []
         # cross-step pipelining: the previous iteration
         # whose tail the next one overlaps instead of a full step barrier
@@ -278,6 +286,14 @@ class Zo2Engine:
         # data parallel: loss sums are all-reduced before g is formed (K10)
         self.dist_group = None
         self.world = 1
+        # trace (zo2_engine.py:156-159): events of an enqueued iteration are
+        # buffered and delivered by _finish, once the g their update
+        # coefficients depend on is known; _g_last is the g the next deferred
+        # update applies.  trace_update_same_step (MeZOEngine): report each
+        # step's update at that step's end, in RefEngine order (zo_ref.py:97-112)
+        self._tev: list = []
+        self._g_last = 0.0
+        self.trace_update_same_step = False
 
     def _set_k2_grid(self) -> None:
         # K2 grid from occupancy (0) also beside the forward: measured faster
@@ -297,7 +313,9 @@ class Zo2Engine:
         pool = self.runtime.pool
         need = DualForward.estimate_nbytes(self.workload.spec, batch_size,
                                            self.workload.arith, 2)
-        sets = 2 if pool.used + need <= pool.capacity else 1
+        # the current forward's booking is released when it is rebuilt
+        booked = sum(self._booked.values())
+        sets = 2 if pool.used - booked + need <= pool.capacity else 1
         if sets != self.operand_sets:
             self.operand_sets = sets
             self.dev.operand_sets = sets
@@ -342,15 +360,43 @@ class Zo2Engine:
             raise StateCorruptionError(f"pending update for {module} but no saved state (lrs)")
         self.mgr.push_rs(step, module, rs)
         size = self._handles[module].size
-        self._emit("update", module, -(self.cfg.lr * self.pending.g), lrs) if update and size else None
-        self._emit("perturb", module, self.cfg.eps, rs) if size else None
+        if size:
+            if update and not self.trace_update_same_step:
+                self._emit("update", module, _G_PREV, lrs)
+            self._emit_perturbs(module, rs)
         self.mgr.set_state(rs.seed, rs.advanced(size))
         return rs, lrs, update
 
-    def _emit(self, op: str, module: str, coef: float, state: RngState | None) -> None:
+    def _emit(self, op: str, module: str, coef, state: RngState | None) -> None:
+        """Buffer one trace event of the iteration being enqueued; coef may be
+        _G_PREV / _G_CUR (resolved in _finish to -(lr*g) of the previous /
+        this iteration)."""
         if self.trace is not None and state is not None:
-            self.trace({"op": op, "module": module, "coef": coef,
-                        "state": (state.seed, state.stream, state.counter)})
+            self._tev.append((op, module, coef, (state.seed, state.stream, state.counter)))
+
+    def _emit_perturbs(self, module: str, rs: RngState) -> None:
+        """The three perturbation passes of one module visit (zo2_engine.py:
+        195-202): +eps, -2eps, +eps, all from the same state."""
+        eps = self.cfg.eps
+        for c in (eps, -2.0 * eps, eps):
+            self._emit("perturb", module, c, rs)
+
+    def _deliver(self, events, g: float | None) -> None:
+        """Resolve and hand an iteration's buffered events to the trace callback
+        in enqueue order; g None (non-finite losses): no update of this step."""
+        if self.trace is None:
+            return
+        lr = self.cfg.lr
+        for op, module, coef, st in events:
+            if coef is _G_PREV:
+                if self._g_last == 0.0:  # gated off on the device (g == 0)
+                    continue
+                coef = -(lr * self._g_last)
+            elif coef is _G_CUR:
+                if g is None:
+                    continue
+                coef = -(lr * g)
+            self.trace({"op": op, "module": module, "coef": coef, "state": st})
 
     def _k2(self, buf: torch.Tensor, fmt_code: int, module: str, update: int, lrs_seed: int,
             perturb: bool, rs_seed: int, descs, stream) -> None:
@@ -375,6 +421,8 @@ class Zo2Engine:
         if self.update_mode == "naive":
             rs = self.mgr.get_state()
             self.mgr.push_rs(step, module, rs)
+            if self._handles[module].size:
+                self._emit_perturbs(module, rs)
             self.mgr.set_state(rs.seed, rs.advanced(self._handles[module].size))
             return rs, 0, False
         rs, lrs, update = self._visit(module, step)
@@ -442,7 +490,7 @@ class Zo2Engine:
         rs = self.mgr.pop_current(module, step)
         if self._handles[module].size == 0:
             return
-        self._emit("update", module, float("nan"), rs)
+        self._emit("update", module, _G_CUR, rs)
         if module in (EMBED_ID, HEAD_ID):
             buf, code = self.runtime.persistent[module], _lib.F32
         else:
@@ -463,60 +511,84 @@ class Zo2Engine:
         return arr
 
     def _book_pool(self, fwd: DualForward) -> None:
-        if self._pool_booked:
+        """Book the dual forward's device working set in the DevicePool; a
+        rebuilt forward (new batch size or operand sets) replaces the booking."""
+        if self._booked_fwd is fwd:
             return
+        pool = self.runtime.pool
+        for cat, nb in self._booked.items():
+            pool.free(cat, nb)
+        self._booked, self._booked_fwd = {}, None
         for cat, nb in fwd.nbytes().items():
-            self.runtime.pool.alloc(cat, nb)
-        self._pool_booked = True
+            pool.alloc(cat, nb)
+            self._booked[cat] = nb
+        self._booked_fwd = fwd
 
     # -- one iteration (zo2_engine.py:264-316) --------------------------------
     def step(self, batch, step_index: int) -> float:
         """Reference contract: enqueue the whole iteration, synchronise, return g."""
-        enq, dag, recs = self._enqueue(batch, step_index)
+        enq, dag, recs, events = self._enqueue(batch, step_index)
         self.dev.read_out(self.lanes[Lane.COMPUTE])
         self.lanes.synchronize()
         lp, lm, g, flag = (float(x) for x in self.dev.h_out.tolist())
-        return self._finish(step_index, enq, dag, recs, lp, lm, g, flag)
+        return self._finish(step_index, enq, dag, recs, lp, lm, g, flag, events)
 
     def step_async(self, step_index: int, batch=None) -> None:
         """Enqueue one iteration without waiting (device-resident batch when
         `batch` is None).  The next iteration's deferred update reads g from
         HBM and is gated on g != 0 on the device; drain() synchronises and
         performs the per-step checks of step()."""
-        enq, dag, recs = self._enqueue(batch, step_index)
+        enq, dag, recs, events = self._enqueue(batch, step_index)
         slot = len(self._async)
         if slot >= self._hist.shape[0]:
             raise RuntimeError("too many outstanding async steps; call drain()")
         with torch.cuda.stream(self.lanes[Lane.COMPUTE]):
             self._hist[slot, :3].copy_(self.dev.d_out)
             self._hist[slot, 3:4].copy_(self.dev.d_flag.to(torch.float64))
-        self._async.append((step_index, enq, dag, recs))
+        self._async.append((step_index, enq, dag, recs, events))
         if self.update_mode != "naive":
             self.pending.valid, self.pending.g = True, float("nan")  # resolved on device
 
     def drain(self) -> list[float]:
+        """Synchronise and run the per-step checks of every iteration enqueued
+        by step_async, in order.  If one of them fails (non-finite losses, a
+        scheduling violation) the error names that step; the iterations queued
+        after it already ran with g = 0 on the device (K10 zeroes g on a
+        non-finite loss, so their deferred updates were gated off) and are
+        discarded, and the pending gradient is cleared to match the device."""
         self.lanes.synchronize()
         hist = self._hist[: len(self._async)].cpu().tolist()
         gs = []
-        for (j, enq, dag, recs), (lp, lm, g, flag) in zip(self._async, hist):
-            gs.append(self._finish(j, enq, dag, recs, lp, lm, g, flag))
-        self._async.clear()
+        entries, self._async = self._async, []
+        try:
+            for (j, enq, dag, recs, events), (lp, lm, g, flag) in zip(entries, hist):
+                gs.append(self._finish(j, enq, dag, recs, lp, lm, g, flag, events))
+        except Exception:
+            self.pending.clear()
+            self._g_last = 0.0
+            self.dev.d_out[2].zero_()
+            self._prev_enq = None
+            raise
         return gs
 
-    def _finish(self, step_index, enq, dag, recs, lp, lm, g, flag) -> float:
+    def _finish(self, step_index, enq, dag, recs, lp, lm, g, flag, events=()) -> float:
         timeline = enq.timeline()
         self.runtime.commit_records(timeline, recs)
         if flag != 0.0 or not (math.isfinite(lp) and math.isfinite(lm)):
+            self._deliver(events, None)
             raise NonFiniteLossError(f"step {step_index}: l+={lp}, l-={lm}")
         if self.validate:
             bad = validate_timeline(timeline, dag, tol=2e-6)
             if bad:
                 raise SchedulingContractError("; ".join(str(v) for v in bad[:5]))
         self.timelines.append((step_index, timeline))
+        self._deliver(events, g)
         if self.update_mode == "naive":
             self.pending.clear()
+            self._g_last = 0.0
         else:
             self.pending.set(g)
+            self._g_last = g
         self.losses.append(lp)
         self.losses_minus.append(lm)
         self.gs.append(g)
@@ -573,7 +645,12 @@ class Zo2Engine:
         if len(self.mgr.rsb) != expected:
             raise StateCorruptionError(f"rsb holds {len(self.mgr.rsb)} entries, "
                                        f"expected {expected}")
-        return enq, dag, rt.take_records()
+        if self.trace_update_same_step and not naive:
+            for e in self.mgr.rsb:  # this iteration's states, module order
+                if self._handles[e.module].size:
+                    self._emit("update", e.module, _G_CUR, e.state)
+        events, self._tev = self._tev, []
+        return enq, dag, rt.take_records(), events
 
     def _carry(self):
         """Cross-step edges replacing the per-step barrier (None: barrier);
@@ -589,6 +666,7 @@ class Zo2Engine:
         externally supplied value (e.g. the reference's g for this step), so the
         next step's deferred update -- and finalize -- use exactly it."""
         self.pending.set(g)
+        self._g_last = float(g)
         self.dev.d_out[2].fill_(float(g))
         torch.cuda.synchronize(self.runtime.device)
 
@@ -614,27 +692,31 @@ class Zo2Engine:
                 lrs = self.mgr.lrs_map.get(module)
                 if lrs is None:
                     raise StateCorruptionError(f"finalize: no lrs for {module}")
+                if self.trace is not None and not self.trace_update_same_step:
+                    self.trace({"op": "update", "module": module,
+                                "coef": -(self.cfg.lr * self.pending.g),
+                                "state": (lrs.seed, lrs.stream, lrs.counter)})
                 descs = self._update_descs(module)
                 if h.transferable and getattr(rt, "resident", False):
                     # resident blocks (MeZO): the 'host master' is the device bucket
-                    self._k2(rt.host[module], rt.wire_fmt.code, module, 1, lrs.seed, False, 0,
+                    self._k2(rt.masters[module], rt.wire_fmt.code, module, 1, lrs.seed, False, 0,
                              descs, comp)
                 elif h.transferable:
                     slot = 0
                     with torch.cuda.stream(comp):
-                        rt.slots[slot].copy_(rt.host[module], non_blocking=True)
+                        rt.slots[slot].copy_(rt.masters[module], non_blocking=True)
                     self._k2(rt.slots[slot], rt.wire_fmt.code, module, 1, lrs.seed, False, 0,
                              descs, comp)
                     with torch.cuda.stream(comp):
                         if shard is None:
-                            rt.host[module].copy_(rt.slots[slot], non_blocking=True)
+                            rt.masters[module].copy_(rt.slots[slot], non_blocking=True)
                         else:
                             # write back only this rank's shard: another rank
                             # may already have updated its own shard in the
                             # shared master, so the rest of this copy may hold
                             # a twice-updated region
                             lo, hi = shard[3], shard[4]
-                            rt.host[module][lo:hi].copy_(rt.slots[slot][lo:hi],
+                            rt.masters[module][lo:hi].copy_(rt.slots[slot][lo:hi],
                                                          non_blocking=True)
                     comp.synchronize()
                 else:
@@ -645,6 +727,7 @@ class Zo2Engine:
                 import torch.distributed as dist
                 dist.barrier(group=shard[2])  # all shards written before export
         self.pending.clear()
+        self._g_last = 0.0
         self.mgr.rsb.clear()
         self._prev_enq = None
         return rt.export_params()
@@ -676,6 +759,8 @@ class MeZOEngine:
                                        device=device)
         k = self.runtime.k_slots
         self._engine = Zo2Engine(workload, cfg, self.runtime, overlap=k >= 3, trace=trace, rng=rng)
+        # RefEngine reports each step's update at the end of that step
+        self._engine.trace_update_same_step = True
 
     @property
     def losses(self) -> list[float]:

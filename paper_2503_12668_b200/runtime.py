@@ -261,6 +261,67 @@ def params_digest(params) -> str:
     return h.hexdigest()
 
 
+class HostBlockStore:
+    """Master copy of one block on the host tier (runtime.py:145-199 surface).
+
+    The bytes are the runtime's pinned master (`runtime.masters[module]`):
+    the f32 block itself, or its encoded low-bit copy with a wire codec.
+    Transfers move those bytes unchanged (the codec is decoded / re-encoded
+    on the device inside K2), so load_into / store_from are plain copies of
+    wire-format bytes; apply() edits the master in full precision."""
+
+    def __init__(self, runtime: "OffloadRuntime", module: str):
+        self._rt, self.module = runtime, module
+        self.codec = runtime.codec
+
+    @property
+    def tensor(self) -> torch.Tensor:
+        return self._rt.masters[self.module]
+
+    @property
+    def nbytes(self) -> int:
+        t = self.tensor
+        return t.numel() * t.element_size()
+
+    @property
+    def wire_fmt(self) -> ElemFormat:
+        return self._rt.wire_fmt
+
+    def load_into(self, arena: torch.Tensor) -> None:
+        arena.copy_(self.tensor)
+
+    def store_from(self, arena: torch.Tensor) -> None:
+        self.tensor.copy_(arena)
+
+    def apply(self, fn) -> None:
+        """runtime.py:186-193: fn(flat) mutates the master as an f32 (or f64)
+        numpy array; with a codec the master is decoded on the device, edited,
+        and re-encoded (conversions counted like every other encode)."""
+        rt = self._rt
+        torch.cuda.synchronize(rt.device)
+        if self.codec is None:
+            if self.tensor.device.type == "cpu":
+                fn(self.tensor.numpy())
+            else:
+                flat = self.tensor.cpu().numpy()
+                fn(flat)
+                self.tensor.copy_(torch.from_numpy(flat))
+            return
+        s = torch.cuda.current_stream(rt.device).cuda_stream
+        enc = self.tensor.to(rt.device)
+        wide = torch.empty(enc.numel(), dtype=torch.float32, device=rt.device)
+        _lib.call("zo2_decode", enc.data_ptr(), wide.data_ptr(), self.codec.code, enc.numel(), s)
+        flat = wide.cpu().numpy()
+        fn(flat)
+        wide.copy_(torch.from_numpy(flat))
+        _lib.call("zo2_encode", wide.data_ptr(), enc.data_ptr(), self.codec.code, enc.numel(),
+                  rt.d_conv.data_ptr(), s)
+        self.tensor.copy_(enc)
+        torch.cuda.synchronize(rt.device)
+        nan, sat = (int(x) for x in rt.d_conv.tolist())
+        rt.conversion.nan_count, rt.conversion.saturated_count = nan, sat
+
+
 class OffloadRuntime:
     """Pinned host masters + K device arenas + transfer log + pool, for one run
     (runtime.py:202-304 surface)."""
@@ -283,14 +344,14 @@ class OffloadRuntime:
         self.block_size = module_size(self.spec, block_id(0)) if self._block_ids else 0
         self.d_conv = torch.zeros(2, dtype=torch.int64, device=self.device)
         sdt = _TORCH_STORAGE[self.wire_fmt]
-        # host stores (HostBlockStore): alias the f32 masters, or encode them
-        self.host: dict[str, torch.Tensor] = {}
+        # pinned host masters: alias the f32 blocks, or encode them
+        self.masters: dict[str, torch.Tensor] = {}
         if params.block_codec is not None and params.block_codec is not self.codec:
             raise ValueError(f"blocks were initialised as {params.block_codec.tag}, runtime "
                              f"codec is {self.codec.tag if self.codec else 'none'}")
         if self.codec is None or params.block_codec is self.codec:
             for i, b in enumerate(self._block_ids):
-                self.host[b] = params.blocks[i]
+                self.masters[b] = params.blocks[i]
             if params.init_conversion is not None:
                 self.d_conv += params.init_conversion
         else:
@@ -303,9 +364,11 @@ class OffloadRuntime:
                           self.block_size, self.d_conv.data_ptr(), s)
                 host = torch.empty(self.block_size, dtype=sdt, pin_memory=True)
                 host.copy_(enc)
-                self.host[b] = host
+                self.masters[b] = host
             del scratch, enc
             torch.cuda.synchronize()
+        # the reference's per-block host stores (runtime.py:145-199) over them
+        self.host = {b: HostBlockStore(self, b) for b in self._block_ids}
         # persistent residents: embedding and LM head (f32, never evicted)
         self.persistent = {EMBED_ID: params.embedding, HEAD_ID: params.lm_head}
         for t in self.persistent.values():
@@ -382,41 +445,48 @@ class OffloadRuntime:
         return self.slots[slot]
 
     def host_param_bytes(self) -> int:
-        return sum(t.numel() * t.element_size() for t in self.host.values())
+        return sum(t.numel() * t.element_size() for t in self.masters.values())
 
     # -- transfers (enqueue only; times are filled from CUDA events) --------
     def upload(self, module: str, slot: int, step: int, stream: torch.cuda.Stream,
-               key: str | None = None) -> None:
+               key: str | None = None) -> TransferRecord:
+        """runtime.py:255-270.  Returns the step's TransferRecord; the copy is
+        only enqueued on `stream`, so t_start / t_end are stamped with the
+        device times of its CUDA events when the step's timeline is committed
+        (commit_records) -- the same object, updated in place."""
         if self._slot_owner[slot] is not None:
             raise SchedulingContractError(
                 f"upload of {module} into slot {slot} still owned by "
                 f"{self._slot_owner[slot]} (scheduler bug)")
         with torch.cuda.stream(stream):
             if self.shard is None:
-                self.slots[slot].copy_(self.host[module], non_blocking=True)
+                self.slots[slot].copy_(self.masters[module], non_blocking=True)
             else:
                 lo, hi = self.shard[3], self.shard[4]
-                self.slots[slot][lo:hi].copy_(self.host[module][lo:hi], non_blocking=True)
+                self.slots[slot][lo:hi].copy_(self.masters[module][lo:hi], non_blocking=True)
                 self._gather(slot)
         self._slot_owner[slot] = module
         rec = TransferRecord(module, "upload", self.wire_nbytes, self.wire_fmt, 0.0, 0.0, step)
         self._pending_records.append((rec, key or f"U:{module}"))
+        return rec
 
     def offload(self, module: str, slot: int, step: int, stream: torch.cuda.Stream,
-                key: str | None = None) -> None:
+                key: str | None = None) -> TransferRecord:
+        """runtime.py:272-285; see upload() for the record's timestamps."""
         if self._slot_owner[slot] != module:
             raise SchedulingContractError(
                 f"offload of {module} from slot {slot} owned by {self._slot_owner[slot]} "
                 f"(scheduler bug)")
         with torch.cuda.stream(stream):
             if self.shard is None:
-                self.host[module].copy_(self.slots[slot], non_blocking=True)
+                self.masters[module].copy_(self.slots[slot], non_blocking=True)
             else:
                 lo, hi = self.shard[3], self.shard[4]
-                self.host[module][lo:hi].copy_(self.slots[slot][lo:hi], non_blocking=True)
+                self.masters[module][lo:hi].copy_(self.slots[slot][lo:hi], non_blocking=True)
         self._slot_owner[slot] = None
         rec = TransferRecord(module, "offload", self.wire_nbytes, self.wire_fmt, 0.0, 0.0, step)
         self._pending_records.append((rec, key or f"O:{module}"))
+        return rec
 
     def take_records(self) -> list:
         out, self._pending_records = self._pending_records, []
@@ -440,14 +510,14 @@ class OffloadRuntime:
             s = torch.cuda.current_stream().cuda_stream
             decoded = []
             for i, b in enumerate(self._block_ids):
-                enc.copy_(self.host[b])
+                enc.copy_(self.masters[b])
                 _lib.call("zo2_decode", enc.data_ptr(), scratch.data_ptr(), self.codec.code,
                           self.block_size, s)
                 if self.params.block_codec is None:
                     self.params.blocks[i].copy_(scratch)
                 else:  # blocks alias the encoded masters: export into fresh f32 copies
                     decoded.append(scratch.cpu())
-            if decoded:  # the runtime keeps its encoded masters in self.host
+            if decoded:  # the runtime keeps its encoded masters in self.masters
                 self.params.blocks = decoded
                 self.params.block_codec = None
             torch.cuda.synchronize()
@@ -491,7 +561,8 @@ class ResidentRuntime(OffloadRuntime):
             self.pool.alloc("persistent_params", t.numel() * 4)
         self.pool.alloc("resident_blocks", len(self._block_ids) * self.block_nbytes)
         self.slots = [b.to(self.device) for b in params.blocks]
-        self.host = {b: self.slots[i] for i, b in enumerate(self._block_ids)}
+        self.masters = {b: self.slots[i] for i, b in enumerate(self._block_ids)}
+        self.host = {b: HostBlockStore(self, b) for b in self._block_ids}
         self._slot_owner = [None] * self.k_slots
         self._pending_records = []
 

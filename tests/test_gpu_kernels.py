@@ -275,6 +275,87 @@ def test_update_perturb_full_size_codec_block(cuda, dim, codec):
     assert torch.equal(op.hi.view(-1), wq.view(-1).to(torch.bfloat16))
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("coef,counter", [(1e-3, 0), (-2e-3, 2**40 + 1), (-2.5e-7, 2**64 - 1000)])
+def test_axpy_z_vs_oracle(cuda, oracle, dtype, coef, counter):
+    """zo2_axpy_z (the reference-order single pass, model.py:227-233) against
+    the oracle's axpy_z on 2^20 + 5 elements: weights over ten decades plus
+    NaN / +-inf / +-0 / subnormal / near-overflow entries; bit-identical."""
+    n = (1 << 20) + 5
+    w = _scaled_weights(n, 3).astype(dtype)
+    w[:8] = [np.nan, np.inf, -np.inf, 0.0, -0.0, 1e-41, 3.4e38, -3.4e38]
+    dev = torch.from_numpy(w.copy()).to(cuda)
+    fmt = L().F32 if dtype == np.float32 else L().F64
+    L().call("zo2_axpy_z", dev.data_ptr(), fmt, n, coef, 0xC0FFEE, 0, counter, stream())
+    ref = w.copy()
+    oracle.axpy_z(ref, coef, 0xC0FFEE, counter)
+    got = dev.cpu().numpy()
+    u = np.uint64 if dtype == np.float64 else np.uint32
+    bad = np.nonzero(got.view(u) != ref.view(u))[0]
+    assert bad.size == 0, f"{bad.size} differ, first {bad[:5]} {got[bad[:3]]} {ref[bad[:3]]}"
+
+
+@pytest.mark.parametrize("dim,codec", [(7168, "bf16"), (12288, "f16")])
+def test_update_perturb_full_size_block_vs_oracle(cuda, oracle, dim, codec):
+    """BASELINE sizes against the ORACLE (not the library's own passes): a whole
+    OPT-30B block (cfg4, bf16 wire) and a whole OPT-175B block (cfg5, f16 wire)
+    through K2 on the codec arena, then >= 1.2 M positions checked with the
+    oracle's z: 2^20 uniformly sampled positions plus every position of a
+    further 2^22-sample whose perturbation z is on ndtri's tail branch
+    (|z| > 1.1, y < exp(-2)) -- decode, the deferred update at lr*g, +eps,
+    -2eps, +eps in f32 with one rounding each, encode: arena codes identical,
+    and the W+ operand of qkv_w identical where the sample hits it."""
+    from paper_2503_12668_b200.model import (DualForward, ModelSpec, block_layout, module_size,
+                                             segments)
+    _l = L()
+    spec = ModelSpec(1, dim, dim // 128, 50272, 512)
+    fwd = DualForward(spec, 1, "bf16", cuda, 1)
+    n = module_size(spec, "block.0")
+    base, lrs, rs, eps, lr, g = 30_000_000_000, 0x5EED, 0xBEEF, 1e-3, 1e-4, -2.5
+    tdt = torch.bfloat16 if codec == "bf16" else torch.float16
+    fmt = _l.BF16 if codec == "bf16" else _l.F16
+    gen = torch.Generator(device=cuda).manual_seed(13)
+    arena = torch.empty(n, dtype=tdt, device=cuda)
+    for i in range(0, n, 1 << 28):
+        j = min(n, i + (1 << 28))
+        arena[i:j] = (torch.randn(j - i, device=cuda, generator=gen) * 0.02).to(tdt)
+    rng = np.random.default_rng(dim)
+    uni = rng.choice(n, 1 << 20, replace=False)
+    cand = rng.choice(n, 1 << 22, replace=False)
+    zc = oracle.gauss_at(rs, 0, base, cand.astype(np.uint64))
+    tail = cand[np.abs(zc) > 1.1]
+    idx = np.unique(np.concatenate([uni, tail]))
+    assert idx.size >= 1_200_000
+    t_idx = torch.from_numpy(idx).to(cuda)
+    src_bits = arena[t_idx].view(torch.int16).cpu().numpy().view(np.uint16)
+    d_g = torch.tensor([g], dtype=torch.float64, device=cuda)
+    counts = torch.zeros(2, dtype=torch.int64, device=cuda)
+    descs = fwd.block_descs(0)
+    _l.call("zo2_update_perturb", arena.data_ptr(), fmt, n, base, 1, d_g.data_ptr(), lr, lrs,
+            1, eps, rs, descs, len(descs), counts.data_ptr(), stream())
+    torch.cuda.synchronize()
+    got = arena[t_idx].view(torch.int16).cpu().numpy().view(np.uint16)
+    u = idx.astype(np.uint64)
+    w = oracle.decode(src_bits, codec)
+    w = oracle.axpy_z_at(w, u, -(lr * g), lrs, base)
+    wp = oracle.axpy_z_at(w, u, eps, rs, base)
+    w = oracle.axpy_z_at(wp, u, -2.0 * eps, rs, base)
+    w = oracle.axpy_z_at(w, u, eps, rs, base)
+    ref_bits = oracle.encode(w, codec)[0]
+    bad = np.nonzero(got != ref_bits)[0]
+    assert bad.size == 0, f"{bad.size} of {idx.size} sampled positions differ, first {idx[bad[:5]]}"
+    assert counts.cpu().tolist() == [0, 0]
+    qkv = [sg for sg in segments(block_layout(spec)) if sg.name == "qkv_w"][0]
+    rows, cols = qkv.shape
+    inq = (idx >= qkv.offset) & (idx < qkv.offset + qkv.size)
+    r, c = np.divmod(idx[inq] - qkv.offset, cols)
+    op = fwd.sets[0][1]["qkv_w"][0].hi.view(cols, rows)
+    got_op = op[torch.from_numpy(c).to(cuda), torch.from_numpy(r).to(cuda)]
+    want_op = torch.from_numpy(wp[inq]).to(torch.bfloat16)
+    assert inq.sum() > 100_000
+    assert torch.equal(got_op.cpu().view(torch.int16), want_op.view(torch.int16))
+
+
 # ------------------------------------------------------------------ K2c
 def test_zapprox_bound_exhaustive(cuda):
     """The certified K2 path's error bound tau(z~) (zo2_zapprox.cuh) holds for

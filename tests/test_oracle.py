@@ -109,3 +109,18 @@ def test_perturb_restore_drift_bounded(oracle):
     z = oracle.gauss(77, 0, 0, w.size)
     inter = np.maximum(np.abs(w0), np.abs(w0) + eps * np.abs(z)).astype(np.float32)
     assert np.max(np.abs(w - w0) / np.spacing(inter)) <= 4.0
+
+
+def test_gauss_at_matches_fill(oracle):
+    """Sampled-position z (used by the whole-block K2 checks) equals the
+    sequential fill at the same positions, across Philox block boundaries."""
+    n, ctr = 4099, 2**40 + 3
+    full = oracle.gauss(77, 0, ctr, n)
+    idx = np.random.default_rng(0).choice(n, 600, replace=False).astype(np.uint64)
+    assert np.array_equal(oracle.gauss_at(77, 0, ctr, idx).view(np.uint64),
+                          full[idx.astype(np.int64)].view(np.uint64))
+    w = np.random.default_rng(1).standard_normal(n).astype(np.float32)
+    seq = w.copy()
+    oracle.axpy_z(seq, -3e-3, 77, ctr)
+    at = oracle.axpy_z_at(w[idx.astype(np.int64)], idx, -3e-3, 77, ctr)
+    assert np.array_equal(at.view(np.uint32), seq[idx.astype(np.int64)].view(np.uint32))

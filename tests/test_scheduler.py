@@ -163,9 +163,9 @@ def test_operand_set_choice_follows_capacity():
     assert two > one > 0
     calls = []
 
-    def fake(cap, auto=True, used=1000):
+    def fake(cap, auto=True, used=1000, booked=0):
         eng = SimpleNamespace(
-            _sets_auto=auto, operand_sets=2,
+            _sets_auto=auto, operand_sets=2, _booked={"activations": booked},
             dev=SimpleNamespace(fwd=None, operand_sets=2),
             runtime=SimpleNamespace(pool=SimpleNamespace(used=used, capacity=cap)),
             workload=SimpleNamespace(spec=spec, arith="f32"),
@@ -177,3 +177,5 @@ def test_operand_set_choice_follows_capacity():
     assert fake(1000 + two - 1) == (1, 1)
     assert fake(1000 + one) == (1, 1)
     assert fake(1000 + one, auto=False) == (2, 2)
+    # the current forward's own booking does not count against its rebuild
+    assert fake(1000 + two, used=1000 + 500, booked=500) == (2, 2)
