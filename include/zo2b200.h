@@ -252,6 +252,33 @@ int zo2_attention(const void *qkv_hi, const void *qkv_lo, uint32_t batch,
                   uint32_t seq, uint32_t n_heads, uint32_t head_dim,
                   void *ctx_hi, void *ctx_lo, void *cuda_stream);
 
+/* ======================= f64 forward (arith=f64) ========================
+ * The reference's default arithmetic (harness/config.py:53): the forward of
+ * model.py:241-313 in IEEE binary64, run by the engine between in-place
+ * perturbation passes (zo2_axpy_z), exactly the reference's per-module
+ * sequence (zo2_engine.py:183-204).  Row-major f64 tensors throughout. */
+#define ZO2_F64_EPI_STORE 0     /* C = A@B + bias                          */
+#define ZO2_F64_EPI_GELU 1      /* C = gelu_erf(A@B + bias)   (model.py _gelu) */
+#define ZO2_F64_EPI_RESIDUAL 2  /* C = C + (A@B + bias)       (h + (x@W + b)) */
+/* C[M,N] from A[M,K] and B [K,N] (b_trans 0) or [N,K] (b_trans 1: A@B^T,
+ * the head's h @ W^T, model.py:301); bias [N] or NULL. */
+int zo2_f64_gemm(const double *A, const double *B, int b_trans, const double *bias,
+                 double *C, uint64_t M, uint64_t N, uint64_t K, int epi, void *cuda_stream);
+/* model.py:259-262 _ln: (x - mean) / sqrt(var + 1e-5) * g + b per row. */
+int zo2_f64_layernorm(const double *x, uint64_t rows, uint32_t dim, const double *gamma,
+                      const double *beta, double *out, void *cuda_stream);
+/* model.py:251-261: out[t] = tok_emb[ids[t]] + pos_emb[t % seq]. */
+int zo2_f64_embed(const int64_t *ids, uint64_t n_tok, uint32_t seq, uint32_t dim,
+                  const double *tok_emb, const double *pos_emb, double *out,
+                  void *cuda_stream);
+/* model.py:273-283 causal softmax attention on packed qkv [B*S, 3d] -> ctx [B*S, d]. */
+int zo2_f64_attention(const double *qkv, uint32_t batch, uint32_t seq, uint32_t n_heads,
+                      uint32_t head_dim, double *ctx, void *cuda_stream);
+/* model.py:308-313: row_loss[r] = logsumexp(logits[r]) - logits[r, target[r]],
+ * *d_sum = sum over rows in a fixed order (NaN rows for out-of-range targets). */
+int zo2_f64_ce(const double *logits, const int64_t *targets, uint64_t rows, uint32_t vocab,
+               double *row_loss, double *d_sum, void *cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

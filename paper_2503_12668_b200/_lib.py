@@ -23,6 +23,7 @@ F64, F32, F16, BF16, F8E4M3 = 0, 1, 2, 3, 4
 
 OUT_NONE, OUT_F32, OUT_BF16_T, OUT_SPLIT_T, OUT_BF16, OUT_SPLIT = 0, 1, 2, 3, 4, 5
 EPI_STORE, EPI_RESIDUAL, EPI_GELU, EPI_CE, EPI_OPERAND = 0, 1, 2, 3, 4
+F64_EPI_STORE, F64_EPI_GELU, F64_EPI_RESIDUAL = 0, 1, 2
 CE_PARTS = 148
 
 
@@ -85,6 +86,16 @@ _SIGS = {
     "zo2_attention": (c_int, [c_void_p, c_void_p, c_uint32, c_uint32, c_uint32, c_uint32,
                               c_void_p,
                               c_void_p, c_void_p]),
+    "zo2_f64_gemm": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_uint64, c_uint64,
+                             c_uint64, c_int, c_void_p]),
+    "zo2_f64_layernorm": (c_int, [c_void_p, c_uint64, c_uint32, c_void_p, c_void_p, c_void_p,
+                                  c_void_p]),
+    "zo2_f64_embed": (c_int, [c_void_p, c_uint64, c_uint32, c_uint32, c_void_p, c_void_p,
+                              c_void_p, c_void_p]),
+    "zo2_f64_attention": (c_int, [c_void_p, c_uint32, c_uint32, c_uint32, c_uint32, c_void_p,
+                                  c_void_p]),
+    "zo2_f64_ce": (c_int, [c_void_p, c_void_p, c_uint64, c_uint32, c_void_p, c_void_p,
+                           c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

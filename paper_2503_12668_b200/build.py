@@ -19,7 +19,8 @@ LIBDIR = PKG / "_lib"
 LIBNAME = "libzo2b200.so"
 INCLUDE = PKG.parent / "include"
 
-SOURCES = ["zo2_elementwise.cu", "zo2_k2.cu", "zo2_layers.cu", "zo2_gemm_sm100.cu", "zo2_attention.cu"]
+SOURCES = ["zo2_elementwise.cu", "zo2_k2.cu", "zo2_layers.cu", "zo2_gemm_sm100.cu", "zo2_attention.cu",
+           "zo2_f64.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 EXTRA = os.environ.get("ZO2_NVCC_EXTRA", "").split()
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

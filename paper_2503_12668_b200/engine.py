@@ -26,9 +26,10 @@ import torch
 from . import _lib
 from .errors import (NonFiniteLossError, SchedulingContractError, StateCorruptionError,
                      UsageError)
-from .model import (EMBED_ID, HEAD_ID, DualForward, ModelSpec, module_order, module_size,
-                    rng_offsets)
-from .numerics import BATCH_STREAM, PERTURB_STREAM, RngState, derive_step_seed, raw_uint64
+from .model import (EMBED_ID, HEAD_ID, DualForward, F64Forward, ModelSpec, module_order,
+                    module_size, rng_offsets)
+from .numerics import (BATCH_STREAM, PERTURB_STREAM, ElemFormat, RngState, derive_step_seed,
+                       raw_uint64)
 from .runtime import ModelParams, OffloadRuntime
 from .scheduler import (CudaLanes, Lane, build_iteration_dag, build_prepare_dag, ckey,
                         close_step, cross_step_edges, enqueue_dag, okey, pkey, ukey,
@@ -188,8 +189,11 @@ class _DeviceStep:
         if self.fwd is None or self.fwd.B != batch_size:
             self.fwd = None
             torch.cuda.empty_cache()
-            self.fwd = DualForward(self.spec, batch_size, self.arith, self.device,
-                                   self.operand_sets)
+            if self.arith == "f64":
+                self.fwd = F64Forward(self.spec, batch_size, self.device)
+            else:
+                self.fwd = DualForward(self.spec, batch_size, self.arith, self.device,
+                                       self.operand_sets)
             T = self.fwd.T
             # a ring of pinned staging buffers: step_async may enqueue several
             # iterations before the first one's token copy has executed
@@ -251,6 +255,16 @@ class Zo2Engine:
             raise ValueError("overlap requires at least 3 arena slots")
         if backend != "cuda":
             raise ValueError("this engine runs on the 'cuda' backend only")
+        if workload.arith == "f64":
+            # the reference's default arithmetic: f64 buckets, perturbed in place
+            # around two f64 forwards (no operand emission, so no prepare lane)
+            if runtime.codec is not None:
+                raise UsageError("arith f64 with a wire codec: the reference runs codecs with "
+                                 "f32 arithmetic (harness/config.py:112-113)")
+            if runtime.wire_fmt is not ElemFormat.F64:
+                raise UsageError("arith f64 needs f64 parameters: "
+                                 "init_params(spec, state, ElemFormat.F64)")
+            prepare_lane = False
         self.workload, self.cfg, self.runtime = workload, cfg, runtime
         self.overlap, self.backend, self.update_mode = overlap, backend, update_mode
         self.cost, self.trace, self.validate = cost, trace, validate
@@ -453,8 +467,12 @@ class Zo2Engine:
             fwd.block_forward(s, self._set_of(module))
 
     def _head_tail(self, fwd, stream) -> None:
+        fwd.head_forward(stream.cuda_stream)
+        self._form_g(fwd, stream)
+
+    def _form_g(self, fwd, stream) -> None:
+        """Loss sums (all-reduced under data parallel) -> l+, l-, g on device."""
         s = stream.cuda_stream
-        fwd.head_forward(s)
         if self.dist_group is not None:
             from .parallel import allreduce_loss_sums
             with torch.cuda.stream(stream):
@@ -465,6 +483,9 @@ class Zo2Engine:
     def _compute(self, module: str, step: int, seq: int, stream: torch.cuda.Stream) -> None:
         """Reference-shaped C task: K2 and forward of one module on one lane
         (the embedding always; every module in naive update mode)."""
+        if self.workload.arith == "f64":
+            self._compute_f64(module, step, stream)
+            return
         fwd = self.dev.fwd
         rs, lrs_seed, update = self._bookkeep(module, step)
         s = stream.cuda_stream
@@ -485,6 +506,41 @@ class Zo2Engine:
                      lrs_seed, True, rs.seed, fwd.block_descs(0), stream)
             fwd.block_forward(s, 0)
 
+    def _compute_f64(self, module: str, step: int, stream: torch.cuda.Stream) -> None:
+        """arith=f64: the reference's dual_forward verbatim (zo2_engine.py:
+        183-204) on the device -- deferred update (K2, gated on g != 0 on
+        device), then +eps / forward(+) / -2eps / forward(-) / +eps in place on
+        the f64 bucket, each pass one zo2_axpy_z over the module's z."""
+        fwd = self.dev.fwd
+        rs, lrs_seed, update = self._bookkeep(module, step)
+        rt = self.runtime
+        if module in (EMBED_ID, HEAD_ID):
+            buf = rt.persistent[module]
+        else:
+            buf = rt.slot_bucket(rt.slot_for(self._blocks.index(module)))
+        n = self._handles[module].size
+        s = stream.cuda_stream
+        if n and update:
+            self._k2(buf, _lib.F64, module, 1, lrs_seed, False, 0, self._update_descs(module),
+                     stream)
+        off, eps = self.dev.offsets[module], self.cfg.eps
+
+        def axpy(coef):
+            if n:
+                _lib.call("zo2_axpy_z", buf.data_ptr(), _lib.F64, n, coef, rs.seed, rs.stream,
+                          off, s)
+        axpy(eps)
+        fwd.forward(module, buf, 0, s)
+        axpy(-2.0 * eps)
+        fwd.forward(module, buf, 1, s)
+        axpy(eps)
+        if module == HEAD_ID:
+            self._form_g(fwd, stream)
+
+    @staticmethod
+    def _fmt_of(t: torch.Tensor) -> int:
+        return _lib.F64 if t.dtype == torch.float64 else _lib.F32
+
     def _naive_update(self, module: str, step: int, stream: torch.cuda.Stream) -> None:
         """zo2_engine.py:251-260: update after g with the same-step state (no gate)."""
         rs = self.mgr.pop_current(module, step)
@@ -492,7 +548,8 @@ class Zo2Engine:
             return
         self._emit("update", module, _G_CUR, rs)
         if module in (EMBED_ID, HEAD_ID):
-            buf, code = self.runtime.persistent[module], _lib.F32
+            buf = self.runtime.persistent[module]
+            code = self._fmt_of(buf)
         else:
             buf = self.runtime.slot_bucket(self.runtime.slot_for(self._blocks.index(module)))
             code = self.runtime.wire_fmt.code
@@ -720,8 +777,8 @@ class Zo2Engine:
                                                          non_blocking=True)
                     comp.synchronize()
                 else:
-                    self._k2(rt.persistent[module], _lib.F32, module, 1, lrs.seed, False, 0,
-                             descs, comp)
+                    self._k2(rt.persistent[module], self._fmt_of(rt.persistent[module]), module,
+                             1, lrs.seed, False, 0, descs, comp)
             comp.synchronize()
             if shard is not None:
                 import torch.distributed as dist

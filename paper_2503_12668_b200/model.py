@@ -401,3 +401,84 @@ class DualForward:
         _lib.call("zo2_ce_reduce", self.ce_all.data_ptr(), T, self.n_tiles_v, 2,
                   self.ce_all.shape[1], self.d_ce_work.data_ptr(), self.d_sums.data_ptr(),
                   stream)
+
+
+class F64Forward:
+    """arith=f64 (the reference's default, harness/config.py:53): the forward
+    of one perturbation sign in IEEE binary64 (csrc/zo2_f64.cu), reading the
+    module's bucket in place.  The engine perturbs the bucket around the two
+    forwards exactly as the reference does (+eps, -2eps, +eps with zo2_axpy_z,
+    zo2_engine.py:183-204), so the weights each forward sees are the
+    reference's W +- eps z bit for bit; only summation orders differ."""
+
+    arith = "f64"
+
+    def __init__(self, spec: ModelSpec, batch_size: int, device):
+        self.spec, self.B = spec, int(batch_size)
+        self.dev = torch.device(device)
+        d, V = spec.dim, spec.vocab
+        T = self.T = self.B * spec.seq_len
+
+        def buf(n):
+            return torch.empty(n, dtype=torch.float64, device=self.dev)
+        self.h = [buf(T * d) for _ in range(2)]
+        self.x, self.qkv, self.ctx, self.mid = buf(T * d), buf(T * 3 * d), buf(T * d), buf(T * 4 * d)
+        self.logits, self.row = buf(T * V), buf(T)
+        self.d_sums = torch.zeros(2, dtype=torch.float64, device=self.dev)
+        # tied head: the embedding's perturbed tok_emb of each sign (model.py:367-369)
+        self.stash = [buf(V * d) for _ in range(2)] if spec.tie_lm_head else None
+        self.ids = torch.empty(T, dtype=torch.int64, device=self.dev)
+        self.targets = torch.empty(T, dtype=torch.int64, device=self.dev)
+        self.prof: list | None = None
+        self._off = {sg.name: sg.offset for sg in segments(block_layout(spec))}
+
+    @staticmethod
+    def estimate_nbytes(spec: ModelSpec, batch_size: int) -> int:
+        d, V, T = spec.dim, spec.vocab, int(batch_size) * spec.seq_len
+        n = 2 * T * d + T * (d + 3 * d + d + 4 * d) + T * V + T
+        n += 2 * V * d if spec.tie_lm_head else 0
+        return 8 * n + 2 * T * 8
+
+    def nbytes(self) -> dict[str, int]:
+        act = sum(t.numel() * 8 for t in self.h + [self.x, self.qkv, self.ctx, self.mid,
+                                                    self.logits, self.row])
+        ops = sum(t.numel() * 8 for t in self.stash) if self.stash else 0
+        return {"activations": act, "operands": ops, "io": 2 * self.T * 8}
+
+    def forward(self, module: str, bucket: torch.Tensor, sign: int, stream) -> None:
+        """Forward of `module` for one sign from its (perturbed) f64 bucket."""
+        spec = self.spec
+        d, V, T = spec.dim, spec.vocab, self.T
+        if module == EMBED_ID:
+            p = bucket.data_ptr()
+            _lib.call("zo2_f64_embed", self.ids.data_ptr(), T, spec.seq_len, d, p,
+                      p + V * d * 8, self.h[sign].data_ptr(), stream)
+            if self.stash is not None:
+                self.stash[sign].copy_(bucket[:V * d])
+        elif module == HEAD_ID:
+            w = self.stash[sign] if self.stash is not None else bucket
+            _lib.call("zo2_f64_gemm", self.h[sign].data_ptr(), w.data_ptr(), 1, None,
+                      self.logits.data_ptr(), T, V, d, _lib.F64_EPI_STORE, stream)
+            _lib.call("zo2_f64_ce", self.logits.data_ptr(), self.targets.data_ptr(), T, V,
+                      self.row.data_ptr(), self.d_sums[sign:].data_ptr(), stream)
+        else:
+            self._block(bucket.data_ptr(), sign, stream)
+
+    def _block(self, base: int, sign: int, stream) -> None:
+        spec = self.spec
+        d, T, H = spec.dim, self.T, spec.n_heads
+        o = {k: base + v * 8 for k, v in self._off.items()}
+        h, x = self.h[sign].data_ptr(), self.x.data_ptr()
+        qkv, ctx, mid = self.qkv.data_ptr(), self.ctx.data_ptr(), self.mid.data_ptr()
+        gemm, E = _lib.call, _lib
+        _lib.call("zo2_f64_layernorm", h, T, d, o["ln1_g"], o["ln1_b"], x, stream)
+        gemm("zo2_f64_gemm", x, o["qkv_w"], 0, o["qkv_b"], qkv, T, 3 * d, d, E.F64_EPI_STORE,
+             stream)
+        _lib.call("zo2_f64_attention", qkv, self.B, spec.seq_len, H, spec.head_dim, ctx, stream)
+        gemm("zo2_f64_gemm", ctx, o["attn_out_w"], 0, o["attn_out_b"], h, T, d, d,
+             E.F64_EPI_RESIDUAL, stream)
+        _lib.call("zo2_f64_layernorm", h, T, d, o["ln2_g"], o["ln2_b"], x, stream)
+        gemm("zo2_f64_gemm", x, o["mlp_in_w"], 0, o["mlp_in_b"], mid, T, 4 * d, d,
+             E.F64_EPI_GELU, stream)
+        gemm("zo2_f64_gemm", mid, o["mlp_out_w"], 0, o["mlp_out_b"], h, T, d, 4 * d,
+             E.F64_EPI_RESIDUAL, stream)

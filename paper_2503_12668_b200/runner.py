@@ -19,7 +19,7 @@ import numpy as np
 from .config import RunConfig, build_config
 from .data import gen_synthetic
 from .engine import MeZOEngine, TransformerWorkload, ZOConfig, Zo2Engine, batch_for_step
-from .numerics import RngState
+from .numerics import ElemFormat, RngState
 from .runtime import OffloadRuntime, init_params, params_digest
 
 SUMMARY_COLUMNS = [
@@ -90,7 +90,8 @@ def append_summary_row(path: Path, row: dict) -> None:
 
 def execute_run(cfg: RunConfig, write_artifacts: bool = True, device="cuda") -> MetricsReport:
     spec = cfg.model_spec()
-    params = init_params(spec, RngState(cfg.seed), device=device)
+    fmt = ElemFormat.F64 if cfg.arith == "f64" else ElemFormat.F32  # runner.py:132
+    params = init_params(spec, RngState(cfg.seed), fmt, device=device)
     workload = TransformerWorkload(params, cfg.arith)
     ds = gen_synthetic(cfg.vocab, cfg.seq_len, cfg.n_samples, RngState(cfg.seed), cfg.pattern,
                        cfg.batch_size)

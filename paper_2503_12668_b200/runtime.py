@@ -205,18 +205,23 @@ def init_params(spec: ModelSpec, state: RngState, fmt: ElemFormat = ElemFormat.F
 
     With `host_masters` (data parallel, one copy per node) the blocks are the
     shared file's views; only its owner writes them."""
-    if fmt is not ElemFormat.F32:
-        raise ValueError("the B200 engine keeps parameters in f32 (arith f32 / bf16)")
+    if fmt not in (ElemFormat.F32, ElemFormat.F64):
+        raise ValueError(f"parameters are f32 (arith f32 / bf16) or f64 (arith f64), "
+                         f"not {fmt.tag}")
+    cfmt = CODEC_FORMATS[codec] if codec not in (None, "none") else None
+    if fmt is ElemFormat.F64 and (cfmt is not None or host_masters is not None):
+        raise ValueError("f64 parameters take no wire codec and no shared masters "
+                         "(the reference's codecs run with f32 arithmetic)")
     seed = state.seed
-    emb = torch.empty(module_size(spec, EMBED_ID), dtype=torch.float32, device=device)
+    dt = torch.float64 if fmt is ElemFormat.F64 else torch.float32
+    emb = torch.empty(module_size(spec, EMBED_ID), dtype=dt, device=device)
     init_module_(spec, EMBED_ID, seed, emb)
-    head = torch.empty(module_size(spec, HEAD_ID), dtype=torch.float32, device=device)
+    head = torch.empty(module_size(spec, HEAD_ID), dtype=dt, device=device)
     if head.numel():
         init_module_(spec, HEAD_ID, seed, head)
-    cfmt = CODEC_FORMATS[codec] if codec not in (None, "none") else None
     blocks = []
     n = module_size(spec, block_id(0))
-    scratch = torch.empty(n, dtype=torch.float32, device=device)
+    scratch = torch.empty(n, dtype=dt, device=device)
     conv = torch.zeros(2, dtype=torch.int64, device=device)
     enc = torch.empty(n, dtype=_TORCH_STORAGE[cfmt], device=device) if cfmt else None
     s = torch.cuda.current_stream().cuda_stream
@@ -229,7 +234,7 @@ def init_params(spec: ModelSpec, state: RngState, fmt: ElemFormat = ElemFormat.F
         init_module_(spec, block_id(i), seed, scratch)
         if cfmt is None:
             if host_masters is None:
-                host = torch.empty(n, dtype=torch.float32, pin_memory=pin)
+                host = torch.empty(n, dtype=dt, pin_memory=pin)
             host.copy_(scratch)
         else:
             _lib.call("zo2_encode", scratch.data_ptr(), enc.data_ptr(), cfmt.code, n,
@@ -372,7 +377,7 @@ class OffloadRuntime:
         # persistent residents: embedding and LM head (f32, never evicted)
         self.persistent = {EMBED_ID: params.embedding, HEAD_ID: params.lm_head}
         for t in self.persistent.values():
-            self.pool.alloc("persistent_params", t.numel() * 4)
+            self.pool.alloc("persistent_params", t.numel() * t.element_size())
         # K arenas in wire format
         self.pool.alloc("block_arenas", self.k_slots * self.block_nbytes)
         self.slots = [torch.empty(self.block_size, dtype=sdt, device=self.device)
@@ -558,7 +563,7 @@ class ResidentRuntime(OffloadRuntime):
         self.d_conv = torch.zeros(2, dtype=torch.int64, device=self.device)
         self.persistent = {EMBED_ID: params.embedding, HEAD_ID: params.lm_head}
         for t in self.persistent.values():
-            self.pool.alloc("persistent_params", t.numel() * 4)
+            self.pool.alloc("persistent_params", t.numel() * t.element_size())
         self.pool.alloc("resident_blocks", len(self._block_ids) * self.block_nbytes)
         self.slots = [b.to(self.device) for b in params.blocks]
         self.masters = {b: self.slots[i] for i, b in enumerate(self._block_ids)}

@@ -17,8 +17,8 @@ def test_defaults_and_overrides(tmp_path):
     assert build_config(None, flat).to_flat() == flat
 
 
-@pytest.mark.parametrize("bad", [{"engine": "x"}, {"backend": "threaded"}, {"codec": "f4"},
-                                 {"arith": "f64"}, {"arena_slots": "2"}, {"steps": "0"},
+@pytest.mark.parametrize("bad", [{"engine": "x"}, {"backend": "mpi"}, {"codec": "f4"},
+                                 {"arith": "f16"}, {"arena_slots": "2"}, {"steps": "0"},
                                  {"n_samples": "0"}, {"nope": "1"}, {"cost.nope": "1"},
                                  {"overlap": "maybe"}, {"ranks": "0"}])
 def test_bad_keys_raise_usage_error(bad):
@@ -37,3 +37,16 @@ def test_model_spec_from_preset():
     cfg = RunConfig(preset="opt-1.3b", seq_len=512)
     s = cfg.model_spec()
     assert (s.n_blocks, s.dim, s.n_heads, s.vocab, s.seq_len) == (24, 2048, 32, 50272, 512)
+
+
+def test_reference_defaults_and_aliases():
+    """The reference's default arith (f64), its f64 -> f32 switch under a codec
+    (harness/config.py:112-113) and its backends accepted as cuda aliases."""
+    assert RunConfig().arith == "f64"
+    assert RunConfig(codec="bf16").arith == "f32"
+    assert RunConfig(codec="bf16", arith="bf16").arith == "bf16"
+    with pytest.warns(UserWarning):
+        cfg = build_config(None, {"backend": "threaded"})
+    assert cfg.backend == "cuda"
+    with pytest.warns(UserWarning):
+        assert build_config(None, {"backend": "simulated"}).backend == "cuda"
