@@ -127,6 +127,28 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// L2-aware tile raster.  Tile r of a problem -> (mt, nt), visiting groups of
+// `gm` M-tiles n-major inside a group: the ~#SM tiles in flight at any time
+// then touch about gm A panels and in_flight / gm B panels, instead of one
+// or two A panels and EVERY B panel of the problem (row-major order).  With
+// production shapes both operands exceed L2 (OPT-30B mlp_out: 32 x 28 tiles
+// of 14.7 MB panels), so what L2 saves is exactly this in-flight sharing.
+__device__ __forceinline__ void tile_mn(uint32_t r, uint32_t tiles_m, uint32_t tiles_n,
+                                        uint32_t gm, uint32_t &mt, uint32_t &nt) {
+  const uint32_t per_group = gm * tiles_n;
+  const uint32_t g = r / per_group, first = g * gm;
+  const uint32_t rows = tiles_m - first < gm ? tiles_m - first : gm;
+  const uint32_t q = r - g * per_group;
+  mt = first + q % rows;
+  nt = q / rows;
+}
+#ifndef ZO2_GEMM_GROUP_M
+#define ZO2_GEMM_GROUP_M 12  // 1-CTA kernel: 148 tiles in flight ~ 12 x 12
+#endif
+#ifndef ZO2_GEMM2_GROUP_M
+#define ZO2_GEMM2_GROUP_M 8  // CTA-pair kernel: 74 tiles in flight ~ 8 x 9
+#endif
+
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row atoms 1024 B apart.
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) |
@@ -324,8 +346,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_gemm(const __grid_constant__
         mbar_arrive(&qfull[qs]);
         if (t >= tiles) break;
         const uint32_t p = t / (tiles_m * tiles_n);
-        const uint32_t r = t % (tiles_m * tiles_n);
-        const int m0 = (int)((r / tiles_n) * BM), n0 = (int)((r % tiles_n) * BN);
+        uint32_t mt, nt;
+        tile_mn(t % (tiles_m * tiles_n), tiles_m, tiles_n, ZO2_GEMM_GROUP_M, mt, nt);
+        const int m0 = (int)(mt * BM), n0 = (int)(nt * BN);
         for (uint32_t kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t *st = smem + stage * C::STAGE_BYTES;
@@ -405,8 +428,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_gemm(const __grid_constant__
       if (lane == 0) mbar_arrive(&qempty[qs]);
       if (t >= tiles) break;
       const uint32_t p = t / (tiles_m * tiles_n);
-      const uint32_t r = t % (tiles_m * tiles_n);
-      const uint32_t mt = r / tiles_n, nt = r % tiles_n;
+      uint32_t mt, nt;
+      tile_mn(t % (tiles_m * tiles_n), tiles_m, tiles_n, ZO2_GEMM_GROUP_M, mt, nt);
       const uint32_t m0 = mt * BM, n0 = nt * BN;
       const uint32_t row = m0 + quad * 32 + lane;
       mbar_wait(&tfull[acc], acc_phase);
@@ -563,9 +586,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       for (uint32_t t = cid; t < tiles; t += ncl) {
         const uint32_t p = t / (tiles_m * tiles_n);
-        const uint32_t r = t % (tiles_m * tiles_n);
-        const int m0 = (int)((r / tiles_n) * 2 * BM + rank * BM);
-        const int n0 = (int)((r % tiles_n) * BN + rank * (BN / 2));
+        uint32_t mt, nt;
+        tile_mn(t % (tiles_m * tiles_n), tiles_m, tiles_n, ZO2_GEMM2_GROUP_M, mt, nt);
+        const int m0 = (int)(mt * 2 * BM + rank * BM);
+        const int n0 = (int)(nt * BN + rank * (BN / 2));
         for (uint32_t kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t *st = smem + stage * C::STAGE_BYTES;
@@ -636,8 +660,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     uint32_t acc_phase = 0;
     for (uint32_t t = cid; t < tiles; t += ncl) {
       const uint32_t p = t / (tiles_m * tiles_n);
-      const uint32_t r = t % (tiles_m * tiles_n);
-      const uint32_t m0 = (r / tiles_n) * 2 * BM + rank * BM, n0 = (r % tiles_n) * BN;
+      uint32_t mt, nt;
+      tile_mn(t % (tiles_m * tiles_n), tiles_m, tiles_n, ZO2_GEMM2_GROUP_M, mt, nt);
+      const uint32_t m0 = mt * 2 * BM + rank * BM, n0 = nt * BN;
       const uint32_t row = m0 + quad * 32 + lane;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -1048,6 +1073,12 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
           if (gn >= (uint32_t)SB) mbar_wait(bar_o, (gn - SB) & 1u);
           tc_fence_after();
           issue_qk(gn);
+        } else if (g >= 1) {
+          // last tile: observe phase g - 1 of bar_o before committing phase g,
+          // so no phase of the barrier completes unobserved by this thread
+          // (compute-sanitizer synccheck "missing wait"); P.V(g - 1) and P.V(g)
+          // accumulate into the same TMEM columns and serialise anyway
+          mbar_wait(bar_o, (g - 1) & 1u);
         }
         // P.V(g) once the softmax stored P(g)
         mbar_wait(&bar_p[g % SB], (g / SB) & 1u);

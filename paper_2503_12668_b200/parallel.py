@@ -29,8 +29,11 @@ def shard_indices(seed: int, step_index: int, n_samples: int, per_rank_batch: in
 
 
 def allreduce_loss_sums(sums: torch.Tensor, group=None) -> torch.Tensor:
-    """In-place SUM all-reduce of the [l+ sum, l- sum] f64 pair."""
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    """In-place SUM all-reduce of the [l+ sum, l- sum] f64 pair.  It runs at
+    every world size once data parallel is enabled (at world 1 it is the
+    identity, but the collective -- NCCL on the compute stream -- still
+    executes, so a single-GPU box exercises the multi-rank code path)."""
+    if dist.is_available() and dist.is_initialized():
         dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
     return sums
 

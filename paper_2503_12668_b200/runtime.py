@@ -392,9 +392,10 @@ class OffloadRuntime:
         host-link bytes drop by `world`; every rank's arena still holds the
         whole block, bit-identical across ranks.  Needs block_size % world ==
         0 (d % 8 == 0 and world | 8); returns False (replicated transfers)
-        otherwise."""
+        otherwise.  world == 1 is accepted (the all-gather is the identity) so
+        the sharded path runs end to end on a single GPU."""
         import torch.distributed as dist
-        if world <= 1 or self.block_size % world != 0:
+        if world < 1 or self.block_size % world != 0:
             return False
         n = self.block_size // world
         # a communicator of its own: the arena all-gathers queue behind each

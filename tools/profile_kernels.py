@@ -1,5 +1,7 @@
 """Launch each hot kernel once at the cfg2 (OPT-1.3B, 16x512) shapes, for
-`ncu --set full` captures (tools only; not part of the product path)."""
+`ncu --set full` captures (tools only; not part of the product path).
+PK_DIM selects another width (heads = dim/128 from 4096 up, as OPT)."""
+import os
 import sys
 
 import torch
@@ -7,9 +9,12 @@ import torch
 sys.path.insert(0, ".")
 from paper_2503_12668_b200.model import DualForward, ModelSpec  # noqa: E402
 
+_D = int(os.environ.get("PK_DIM", "2048"))
+_SPEC = (1, _D, _D // 128 if _D >= 4096 else _D // 64, 50272, 512)
+
 
 def main(arith="f32"):
-    spec = ModelSpec(1, 2048, 32, 50272, 512)
+    spec = ModelSpec(*_SPEC)
     fwd = DualForward(spec, 16, arith, "cuda", 1)
     for t in fwd.h:
         t.normal_()
@@ -32,11 +37,10 @@ def main(arith="f32"):
 
 def k2(arith="f32"):
     """One K2 (update + perturb, transposed operands) over a cfg2 block."""
-    import os
     from paper_2503_12668_b200 import _lib
     from paper_2503_12668_b200.model import module_size
     _lib.call("zo2_set_rng_mode", 1 if os.environ.get("ZO2_RNG") == "fast" else 0)
-    spec = ModelSpec(1, 2048, 32, 50272, 512)
+    spec = ModelSpec(*_SPEC)
     fwd = DualForward(spec, 16, arith, "cuda", 1)
     n = module_size(spec, "block.0")
     arena = torch.randn(n, device="cuda") * 0.02
@@ -51,7 +55,7 @@ def k2(arith="f32"):
 
 def head(arith="f32"):
     """Head GEMM with the fused cross-entropy epilogue (K7) + CE reduce."""
-    spec = ModelSpec(1, 2048, 32, 50272, 512)
+    spec = ModelSpec(*_SPEC)
     fwd = DualForward(spec, 16, arith, "cuda", 1)
     for t in fwd.h:
         t.normal_()
@@ -68,7 +72,7 @@ def head(arith="f32"):
 
 def embed(arith="f32"):
     """Embedding gather with the on-the-fly update + perturbation (K8)."""
-    spec = ModelSpec(1, 2048, 32, 50272, 512)
+    spec = ModelSpec(*_SPEC)
     fwd = DualForward(spec, 16, arith, "cuda", 1)
     table = torch.randn((spec.vocab + spec.seq_len) * spec.dim, device="cuda") * 0.02
     fwd.ids.random_(0, spec.vocab)
