@@ -231,6 +231,10 @@ int zo2_gemm_tile_n(int split);
  * and N >= 256, else single-CTA 128-row tiles), 1 single-CTA only, 2 pair
  * whenever legal.  For A/B measurements and tests. */
 int zo2_set_gemm_variant(int variant);
+/* Tile raster: groups of `group_m` M tiles visited n-major (1 = row-major).
+ * Defaults 12 (single-CTA kernel) and 8 (CTA-pair kernel).  For A/B
+ * measurements; results do not depend on it. */
+int zo2_set_gemm_raster(int group_m_cta, int group_m_pair);
 
 /* Combine CE partials into per-problem token sums (f64): sums[b] =
  * sum_t (logsumexp_t - logit_t[target_t])  (model.py:304-313 numerator).

@@ -80,6 +80,7 @@ _SIGS = {
                          c_void_p]),
     "zo2_gemm_tile_n": (c_int, [c_int]),
     "zo2_set_gemm_variant": (c_int, [c_int]),
+    "zo2_set_gemm_raster": (c_int, [c_int, c_int]),
     "zo2_set_attention_variant": (c_int, [c_int]),
     "zo2_ce_reduce": (c_int, [c_void_p, c_uint32, c_uint32, c_int, c_uint64, c_void_p,
                               c_void_p, c_void_p]),

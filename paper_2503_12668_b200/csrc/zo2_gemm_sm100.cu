@@ -34,7 +34,9 @@ void zo2_count_launch(uint64_t n = 1);
 // beside a GEMM CTA) pass the GEMM tests alone but hung in the full step with
 // K2 running concurrently (tools/ab_variants.sh, cfg3); until that is
 // understood only the tested budget is accepted.
+#ifndef ZO2_GEMM_ALLOW_SMALL_BUDGET
 static_assert(ZO2_GEMM_SMEM_KB >= 192, "GEMM staging budgets below 192 KB are not supported");
+#endif
 
 namespace {
 
@@ -51,6 +53,7 @@ struct alignas(64) GemmArgs {
   float *ce_part[2];
   uint32_t M, N, K;
   int batch;
+  uint32_t group_m;        // raster group height in M tiles (tile_mn)
   unsigned int *tile_ctr;  // [0] next tile, [1] CTAs finished (self-resetting)
 };
 
@@ -69,6 +72,33 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+#ifdef ZO2_MBAR_WATCHDOG
+// diagnostic build (tools/build_variant.py ... -DZO2_MBAR_WATCHDOG): a wait
+// that has not completed after 5 s reports where it is stuck and traps
+__device__ __forceinline__ uint64_t wd_now() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __noinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  uint32_t ok = 0;
+  const uint64_t t0 = wd_now();
+  for (uint64_t it = 0; !ok; ++it) {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (!ok && (it & 1023) == 1023 && wd_now() - t0 > 5000000000ull) {
+      printf("ZO2 mbarrier watchdog: block (%d,%d,%d) thread %d smem 0x%x parity %u\n",
+             blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x, smem_u32(b), parity);
+      __trap();
+    }
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -80,6 +110,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#endif
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, uint64_t *bar,
                                             int x, int y) {
   asm volatile(
@@ -148,6 +179,8 @@ __device__ __forceinline__ void tile_mn(uint32_t r, uint32_t tiles_m, uint32_t t
 #ifndef ZO2_GEMM2_GROUP_M
 #define ZO2_GEMM2_GROUP_M 8  // CTA-pair kernel: 74 tiles in flight ~ 8 x 9
 #endif
+// raster group heights in use ([0] 1-CTA, [1] pair); zo2_set_gemm_raster
+uint32_t g_group_m[2] = {ZO2_GEMM_GROUP_M, ZO2_GEMM2_GROUP_M};
 
 // UMMA shared-memory descriptor: K-major, 128B swizzle, 8-row atoms 1024 B apart.
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -347,7 +380,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_gemm(const __grid_constant__
         if (t >= tiles) break;
         const uint32_t p = t / (tiles_m * tiles_n);
         uint32_t mt, nt;
-        tile_mn(t % (tiles_m * tiles_n), tiles_m, tiles_n, ZO2_GEMM_GROUP_M, mt, nt);
+        tile_mn(t % (tiles_m * tiles_n), tiles_m, tiles_n, args.group_m, mt, nt);
         const int m0 = (int)(mt * BM), n0 = (int)(nt * BN);
         for (uint32_t kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -429,7 +462,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1) k_gemm(const __grid_constant__
       if (t >= tiles) break;
       const uint32_t p = t / (tiles_m * tiles_n);
       uint32_t mt, nt;
-      tile_mn(t % (tiles_m * tiles_n), tiles_m, tiles_n, ZO2_GEMM_GROUP_M, mt, nt);
+      tile_mn(t % (tiles_m * tiles_n), tiles_m, tiles_n, args.group_m, mt, nt);
       const uint32_t m0 = mt * BM, n0 = nt * BN;
       const uint32_t row = m0 + quad * 32 + lane;
       mbar_wait(&tfull[acc], acc_phase);
@@ -587,7 +620,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       for (uint32_t t = cid; t < tiles; t += ncl) {
         const uint32_t p = t / (tiles_m * tiles_n);
         uint32_t mt, nt;
-        tile_mn(t % (tiles_m * tiles_n), tiles_m, tiles_n, ZO2_GEMM2_GROUP_M, mt, nt);
+        tile_mn(t % (tiles_m * tiles_n), tiles_m, tiles_n, args.group_m, mt, nt);
         const int m0 = (int)(mt * 2 * BM + rank * BM);
         const int n0 = (int)(nt * BN + rank * (BN / 2));
         for (uint32_t kb = 0; kb < kblocks; ++kb) {
@@ -661,7 +694,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     for (uint32_t t = cid; t < tiles; t += ncl) {
       const uint32_t p = t / (tiles_m * tiles_n);
       uint32_t mt, nt;
-      tile_mn(t % (tiles_m * tiles_n), tiles_m, tiles_n, ZO2_GEMM2_GROUP_M, mt, nt);
+      tile_mn(t % (tiles_m * tiles_n), tiles_m, tiles_n, args.group_m, mt, nt);
       const uint32_t m0 = mt * 2 * BM + rank * BM, n0 = nt * BN;
       const uint32_t row = m0 + quad * 32 + lane;
       mbar_wait(&tfull[acc], acc_phase);
@@ -780,6 +813,7 @@ int launch(const GemmArgs &a, cudaStream_t s) {
   }
   GemmArgs b = a;
   b.tile_ctr = ctrs[dev] + 2 * (seq[dev]++ % kCtrSlots);
+  b.group_m = g_group_m[0];
   k_gemm<BN, SPLIT, EPI><<<grid, NUM_THREADS, C::SMEM, s>>>(b);
   zo2_count_launch();
   ZO2_CHECK_LAUNCH();
@@ -817,7 +851,9 @@ int launch2(const GemmArgs &a, cudaStream_t s) {
   const uint32_t tiles =
       ((a.M + 2 * BM - 1) / (2 * BM)) * ((a.N + C::BN - 1) / C::BN) * (uint32_t)a.batch;
   const uint32_t pairs = tiles < (uint32_t)(g_num_sms / 2) ? tiles : (uint32_t)(g_num_sms / 2);
-  k_gemm2<SPLIT, EPI><<<2 * pairs, NUM_THREADS, C::SMEM, s>>>(a);
+  GemmArgs b = a;
+  b.group_m = g_group_m[1];
+  k_gemm2<SPLIT, EPI><<<2 * pairs, NUM_THREADS, C::SMEM, s>>>(b);
   zo2_count_launch();
   ZO2_CHECK_LAUNCH();
   return ZO2_OK;
@@ -1249,6 +1285,14 @@ extern "C" int zo2_attention_tc(const void *qkv_hi, const void *qkv_lo, uint32_t
 extern "C" int zo2_gemm_tile_n(int split) {
   (void)split;
   return CE_W;  // CE partials are per CE_W columns for every kernel variant
+}
+
+extern "C" int zo2_set_gemm_raster(int group_m_cta, int group_m_pair) {
+  if (group_m_cta < 1 || group_m_cta > 1024 || group_m_pair < 1 || group_m_pair > 1024)
+    return zo2_set_error(ZO2_E_ARG, "zo2_set_gemm_raster: group heights 1..1024");
+  g_group_m[0] = (uint32_t)group_m_cta;
+  g_group_m[1] = (uint32_t)group_m_pair;
+  return ZO2_OK;
 }
 
 extern "C" int zo2_set_gemm_variant(int v) {

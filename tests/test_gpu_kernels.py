@@ -515,6 +515,28 @@ def test_gemm_store_bias(cuda, gemm_variant, split, M, N, K):
 
 
 @pytest.mark.parametrize("split", [False, True])
+def test_gemm_raster_invariant(cuda, gemm_variant, split):
+    """The tile raster (zo2_set_gemm_raster) reorders tiles, never results:
+    every group height gives bit-identical outputs, ragged last groups
+    included (13 x 7 pair tiles / 26 x 13 single-CTA tiles)."""
+    torch.manual_seed(5)
+    M, N, K = 3300, 3300, 192
+    A = torch.randn(2, M, K, device=cuda)
+    B = torch.randn(2, N, K, device=cuda) * 0.05
+    bias = [torch.randn(N, device=cuda) for _ in range(2)]
+    outs = {}
+    try:
+        for gm in (1, 3, 8, 12, 1024):
+            L().call("zo2_set_gemm_raster", gm, gm)
+            outs[gm] = _run_gemm(A, B, bias, L().EPI_STORE, split)
+    finally:
+        L().call("zo2_set_gemm_raster", 12, 8)
+    for gm, o in outs.items():
+        for s in range(2):
+            assert torch.equal(o[s], outs[1][s]), (gm, s)
+
+
+@pytest.mark.parametrize("split", [False, True])
 def test_gemm_residual_and_gelu(cuda, gemm_variant, split):
     torch.manual_seed(1)
     M, N, K = 384, 512, 256
