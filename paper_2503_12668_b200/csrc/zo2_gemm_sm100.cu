@@ -30,13 +30,9 @@ void zo2_count_launch(uint64_t n = 1);
 #ifndef ZO2_GEMM_SMEM_KB
 #define ZO2_GEMM_SMEM_KB 200  // operand staging budget per CTA
 #endif
-// Smaller budgets (2 split / 5 bf16 stages, leaving room for two K2 CTAs
-// beside a GEMM CTA) pass the GEMM tests alone but hung in the full step with
-// K2 running concurrently (tools/ab_variants.sh, cfg3); until that is
-// understood only the tested budget is accepted.
-#ifndef ZO2_GEMM_ALLOW_SMALL_BUDGET
-static_assert(ZO2_GEMM_SMEM_KB >= 192, "GEMM staging budgets below 192 KB are not supported");
-#endif
+// Smaller budgets (2 split / 5 bf16 stages) leave room for K2 CTAs beside a
+// GEMM CTA; they used to hang the CTA-pair kernel's TMEM allocation (fixed by
+// the cluster barrier before tcgen05.alloc.cta_group::2 in k_gemm2).
 
 namespace {
 
@@ -599,17 +595,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         if (SPLIT || (j & 1) == 0)
           asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&args.tm[p][j]) : "memory");
   }
+  // Both CTAs of the pair meet BEFORE the pair allocation (and relinquish
+  // after it, below).  Without this barrier a peer whose warps start late --
+  // its SM still shared with K2 CTAs, which only fit beside a GEMM CTA with a
+  // staging budget below ~190 KB -- issued its tcgen05.alloc.cta_group::2
+  // after the leader's had completed, and that alloc never returned: cuda-gdb
+  // on the hung step showed the leader at the post-alloc cluster barrier,
+  // the peer's warp 1 spinning inside tcgen05.alloc and no other CTA on
+  // either SM (tools/gpu_r2_hang_gdb.sh).
+  __syncthreads();
+  cluster_sync_all();
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "r"((uint32_t)C::TMEM_COLS)
                  : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
   cluster_sync_all();
   tc_fence_after();
+  // Relinquish only once BOTH CTAs of the pair have allocated.  The pair's
+  // relinquish_alloc_permit.cta_group::2 issued while the peer's alloc is
+  // still pending leaves that alloc waiting forever: with a smaller staging
+  // budget K2 CTAs share the SMs, the peer's warps start late, and the
+  // leader used to get there first (cuda-gdb on the hung step: leader at the
+  // cluster barrier, peer warp 1 spinning inside tcgen05.alloc,
+  // tools/gpu_r2_hang_gdb.sh).
+  if (warp == 1)
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {

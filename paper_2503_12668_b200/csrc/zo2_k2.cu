@@ -223,13 +223,49 @@ __device__ __forceinline__ void emit4(const zo2_segment_desc &sg, int kind, uint
   }
 }
 
+#ifndef ZO2_K2_CERT_UPDATE
+#define ZO2_K2_CERT_UPDATE 1
+#endif
+// z~ of the 4 draws of one Philox block (K2c section below)
+__device__ __forceinline__ void za_z4(const uint64_t r[4], float z[4], float tau[4]);
+// The exact z of one raw draw (Cephes ndtri in IEEE double), out of line: the
+// certified update below needs it for ~1e-4 of the elements.
+__device__ __noinline__ double exact_z(uint64_t raw) { return zo2_ndtri(zo2_u53(raw)); }
+
+// Deferred update of one f32 weight, x = f32(f64(w + f64(uc z))) (axpy1),
+// decided from z~ (zo2_zapprox.cuh, |z~ - z| <= tau) when the whole interval
+// of candidate values rounds to one binary32: |uc| = lr |g| is ~1e-7, so
+// |uc| tau ~ 1e-13 against a binary32 ulp of ~1e-9 and almost every element
+// is certified.  Margin: 1.01 |uc| tau plus 2^-50 (|w| + |uc z~|) for the two
+// f64 roundings of the exact chain and of v +- m (each <= 2^-53 relative).
+// Otherwise (non-finite w, y below z~'s range, or an interval straddling a
+// rounding boundary) the element takes the exact z: the same bits as the
+// queued exact path either way.
+__device__ __forceinline__ float upd_cert(float w, double uc, float zt, float tau, uint64_t raw) {
+  if (fabsf(w) <= 3.0e38f && tau < 1.0e30f) {
+    const double zd = (double)zt;
+    const double v = __dadd_rn((double)w, __dmul_rn(uc, zd));
+    const double m = 1.01 * fabs(uc) * (double)tau + 0x1p-50 * (fabs((double)w) + fabs(uc * zd));
+    const float lo = __double2float_rn(v - m), hi = __double2float_rn(v + m);
+    if (__float_as_uint(lo) == __float_as_uint(hi)) return lo;
+  }
+  return axpy1(w, uc, exact_z(raw));
+}
+__device__ __forceinline__ double upd_cert(double w, double uc, float, float, uint64_t raw) {
+  return axpy1(w, uc, exact_z(raw));  // not used: f64 arenas need the exact z
+}
+
 template <int FMT, bool FAST, bool UPD, bool PERT>
 __device__ __forceinline__ void k2_tiles(void *arena, const K2Table &T, const K2Params &P,
                                          const ZxKeys2 &KS,
                                          K2Smem<typename Wire<FMT>::A> &sm, unsigned &nn,
                                          unsigned &ns) {
   typedef typename Wire<FMT>::A A;
-  constexpr int OFF = UPD ? 4 : 0;  // first perturb slot
+  // f32 arenas: the update draw is certified from z~ in P1 (upd_cert) and only
+  // the perturbation draws go through the exact queue (QU = queued update)
+  constexpr bool CU = UPD && !FAST && FMT == ZO2_F32 && ZO2_K2_CERT_UPDATE;
+  constexpr bool QU = UPD && !CU;
+  constexpr int OFF = QU ? 4 : 0;  // first perturb slot
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const double expm2 = 0.13533528323661269189;
   const double one_m = __dsub_rn(1.0, expm2);
@@ -268,6 +304,17 @@ __device__ __forceinline__ void k2_tiles(void *arena, const K2Table &T, const K2
     if (vec) Wire<FMT>::load4(arena, idx, w);
     else
       for (int j = 0; j < cnt; ++j) w[j] = Wire<FMT>::load1(arena, idx + j);
+    if (CU) {
+      // every lane (za_z4 votes across the warp); lanes past the segment end
+      // draw at harmless positions and keep their zeros
+      uint64_t r[4];
+      float zt[4], tau[4];
+      zx_raw4_k(KS.lrs, P.base + idx, r);
+      za_z4(r, zt, tau);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < cnt) w[j] = upd_cert(w[j], P.ucoef, zt[j], tau[j], r[j]);
+    }
 #pragma unroll
     for (int j = 0; j < 4; ++j) W[widx + j] = w[j];
 
@@ -318,7 +365,7 @@ __device__ __forceinline__ void k2_tiles(void *arena, const K2Table &T, const K2
     } else {
     if (cnt > 0) {
       uint64_t r[4];
-      if (UPD) {
+      if (QU) {
         zx_raw4_k(KS.lrs, P.base + idx, r);
 #pragma unroll
         for (int j = 0; j < 4; ++j) classify(j, r[j], j < cnt);
@@ -345,7 +392,7 @@ __device__ __forceinline__ void k2_tiles(void *arena, const K2Table &T, const K2
       unsigned tp = excl & 0xffffu, cp = NSLOT - 1 - (excl >> 16);
       const int zb0 = zslot(0, t), zb1 = zslot(1, t) - NT;  // even / odd k bases
 #pragma unroll
-      for (int k = 0; k < (UPD ? 4 : 0) + (PERT ? 4 : 0); ++k) {
+      for (int k = 0; k < (QU ? 4 : 0) + (PERT ? 4 : 0); ++k) {
         const int zi = ((k & 1) ? zb1 : zb0) + k * NT;
         if ((tmask >> k) & 1u) sm.q[tp++] = (uint16_t)(zi | (((negmask >> k) & 1u) << 15));
         if ((cmask >> k) & 1u) sm.q[cp--] = (uint16_t)zi;
@@ -438,9 +485,9 @@ __device__ __forceinline__ void k2_tiles(void *arena, const K2Table &T, const K2
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         a[i] = W[wi0 + i * wstep];
-        const double zu = UPD ? sm.z[za[i]] : 0.0;
+        const double zu = QU ? sm.z[za[i]] : 0.0;
         const double zp = PERT ? sm.z[za[i] + OFF * NT] : 0.0;
-        chain_fast<UPD, PERT>(a[i], ap[i], am[i], P.ucoef, zu, P.eps, zp);
+        chain_fast<QU, PERT>(a[i], ap[i], am[i], P.ucoef, zu, P.eps, zp);
         // a NaN anywhere in the chain (NaN weight, inf - inf) reaches the
         // restored weight: redo those elements with axpy1's exact NaN rules
         bad |= (i < acnt) && (a[i] != a[i]);
@@ -449,9 +496,9 @@ __device__ __forceinline__ void k2_tiles(void *arena, const K2Table &T, const K2
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           if (i >= acnt || a[i] == a[i]) continue;
-          const double zu = UPD ? sm.z[za[i]] : 0.0;
+          const double zu = QU ? sm.z[za[i]] : 0.0;
           const double zp = PERT ? sm.z[za[i] + OFF * NT] : 0.0;
-          const Chain3<A> c = chain_exact<UPD, PERT, A>(W[wi0 + i * wstep], P.ucoef, zu, P.eps, zp);
+          const Chain3<A> c = chain_exact<QU, PERT, A>(W[wi0 + i * wstep], P.ucoef, zu, P.eps, zp);
           a[i] = c.w;
           ap[i] = c.wp;
           am[i] = c.wm;

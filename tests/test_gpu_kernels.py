@@ -115,6 +115,34 @@ def test_update_perturb_linear_bit_exact(cuda, oracle, dtype, g):
     assert np.array_equal(minus.cpu().numpy(), wm.astype(np.float32))
 
 
+@pytest.mark.parametrize("ucoef", [1e-9, -2.5e-7, 1e-4, -0.3])
+def test_update_perturb_f32_certified_update(cuda, oracle, ucoef):
+    """f32 arenas certify the deferred update's rounding from z~ and take the
+    exact z only where the interval straddles a binary32 boundary (K2
+    upd_cert).  Against the oracle's reference-order passes on 2^20 + 3
+    weights over ten decades plus NaN / +-inf / +-0 / subnormal / near-overflow
+    entries, at |lr g| from 1e-9 (all certified) to 0.3 (mostly exact):
+    arena and both operands bit-identical."""
+    _l = L()
+    n, base, lrs, rs, eps = (1 << 20) + 3, 77_000_001, 0x51, 0x52, 1e-3
+    w = _scaled_weights(n, 9)
+    w[:8] = [np.nan, np.inf, -np.inf, 0.0, -0.0, 1e-41, 3.4e38, -3.39e38]
+    dev = torch.from_numpy(w.copy()).to(cuda)
+    d_g = torch.tensor([1.0], dtype=torch.float64, device=cuda)
+    plus = torch.empty(n, dtype=torch.float32, device=cuda)
+    minus = torch.empty(n, dtype=torch.float32, device=cuda)
+    segs = (_l.SegmentDesc * 1)()
+    segs[0].offset, segs[0].rows, segs[0].cols, segs[0].out_kind = 0, 1, n, _l.OUT_F32
+    segs[0].out_plus, segs[0].out_minus = plus.data_ptr(), minus.data_ptr()
+    # ucoef = -(lr g) with g = 1
+    _l.call("zo2_update_perturb", dev.data_ptr(), _l.F32, n, base, 1, d_g.data_ptr(), -ucoef,
+            lrs, 1, eps, rs, segs, 1, None, stream())
+    wf, wp, wm = _ref_sequence(oracle, w, base, ucoef, lrs, eps, rs)
+    assert np.array_equal(dev.cpu().numpy().view(np.uint32), wf.view(np.uint32))
+    assert np.array_equal(plus.cpu().numpy().view(np.uint32), wp.astype(np.float32).view(np.uint32))
+    assert np.array_equal(minus.cpu().numpy().view(np.uint32), wm.astype(np.float32).view(np.uint32))
+
+
 @pytest.mark.parametrize("split", [False, True])
 def test_update_perturb_transposed_operands(cuda, oracle, split):
     _l = L()
