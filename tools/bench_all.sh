@@ -1,16 +1,18 @@
 #!/bin/bash
 # all bench lines of a round (run under gpurun); JSON lines into gpurun_out/
-R=${R:-r1}
-timeout 900 python bench.py > gpurun_out/${R}_bench_cfg2.json 2> gpurun_out/${R}_bench_cfg2.err
-timeout 900 python bench.py --rng fast --no-cpu-baseline > gpurun_out/${R}_bench_cfg2_fast.json 2> gpurun_out/${R}_bench_cfg2_fast.err
+R=${R:-r2}
+mkdir -p gpurun_out
+nproc > gpurun_out/${R}_host.txt; free -g >> gpurun_out/${R}_host.txt
+timeout 900 python bench.py > gpurun_out/${R}_bench_default.json 2> gpurun_out/${R}_bench_default.err
+timeout 900 python bench.py --config cfg2 --no-cpu-baseline > gpurun_out/${R}_bench_cfg2.json 2> gpurun_out/${R}_bench_cfg2.err
+timeout 900 python bench.py --config cfg2 --rng fast --no-cpu-baseline > gpurun_out/${R}_bench_cfg2_fast.json 2> gpurun_out/${R}_bench_cfg2_fast.err
 timeout 900 python bench.py --config cfg3 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/${R}_bench_cfg3.json 2> gpurun_out/${R}_bench_cfg3.err
 timeout 900 python bench.py --config cfg3 --steps 3 --warmup 3 --no-cpu-baseline --rng fast > gpurun_out/${R}_bench_cfg3_fast.json 2> gpurun_out/${R}_bench_cfg3_fast.err
-timeout 1200 python bench.py --config cfg4 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/${R}_bench_cfg4.json 2> gpurun_out/${R}_bench_cfg4.err
-timeout 1200 python bench.py --config cfg4 --steps 2 --warmup 3 --no-cpu-baseline --rng fast > gpurun_out/${R}_bench_cfg4_fast.json 2> gpurun_out/${R}_bench_cfg4_fast.err
+timeout 1200 python bench.py --config cfg4 --steps 3 --warmup 3 --no-cpu-baseline --rng fast > gpurun_out/${R}_bench_cfg4_fast.json 2> gpurun_out/${R}_bench_cfg4_fast.err
 timeout 600 python bench.py --config cfg1 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/${R}_bench_cfg1.json 2> gpurun_out/${R}_bench_cfg1.err
 timeout 1500 python bench.py --config cfg5 --steps 2 --warmup 2 --no-cpu-baseline > gpurun_out/${R}_bench_cfg5.json 2> gpurun_out/${R}_bench_cfg5.err
 timeout 1500 python bench.py --config cfg5 --steps 2 --warmup 2 --no-cpu-baseline --rng fast > gpurun_out/${R}_bench_cfg5_fast.json 2> gpurun_out/${R}_bench_cfg5_fast.err
-timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${R}_bench_reference.json 2> gpurun_out/${R}_bench_reference.err
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${R}_bench_reference.json 2> gpurun_out/${R}_bench_reference.err
 for f in gpurun_out/${R}_bench_*.json; do python - "$f" <<'PY'
 import json, sys
 try:
