@@ -172,6 +172,9 @@ __device__ __forceinline__ void tile_mn(uint32_t r, uint32_t tiles_m, uint32_t t
 #ifndef ZO2_GEMM_GROUP_M
 #define ZO2_GEMM_GROUP_M 12  // 1-CTA kernel: 148 tiles in flight ~ 12 x 12
 #endif
+#ifndef ZO2_GEMM2_DYNAMIC
+#define ZO2_GEMM2_DYNAMIC 1  // CTA-pair kernel: dynamic tile scheduler (k_gemm2)
+#endif
 #ifndef ZO2_GEMM2_GROUP_M
 #define ZO2_GEMM2_GROUP_M 8  // CTA-pair kernel: 74 tiles in flight ~ 8 x 9
 #endif
@@ -539,6 +542,30 @@ __device__ __forceinline__ void mbar_arrive_leader(uint64_t *bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_rank(uint64_t *bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+__device__ __forceinline__ void st_rank_u32(uint32_t *p, uint32_t v, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(p)), "r"(rank));
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(remote), "r"(v) : "memory");
+}
+// parity wait with cluster-scope acquire (the phase was completed by, or
+// orders data written by, the other CTA of the pair)
+__device__ __forceinline__ void mbar_wait_cl(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
 __host__ __device__ constexpr uint32_t idesc_bf16_m256(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
@@ -567,7 +594,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   uint64_t *empty = full + C::STAGES;
   uint64_t *tfull = empty + C::STAGES;
   uint64_t *tempty = tfull + 2;
-  uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+  uint64_t *qfull = tempty + 2;   // tile-id ring, written by the leader's producer
+  uint64_t *qempty = qfull + 4;   // (leader's copy is the one used)
+  uint32_t *qtile = (uint32_t *)(qempty + 4);
+  uint32_t *tmem_slot = qtile + 4;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cluster_rank();
@@ -576,7 +606,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
   const uint32_t tiles_m = (M + 2 * BM - 1) / (2 * BM), tiles_n = (N + BN - 1) / BN;
   const uint32_t tiles = tiles_m * tiles_n * (uint32_t)args.batch;
   const uint32_t kblocks = (K + BK - 1) / BK;
+#if !ZO2_GEMM2_DYNAMIC
   const uint32_t cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+#endif
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -586,6 +618,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 8);  // 4 epilogue warps in each of the 2 CTAs
+    }
+    for (int q = 0; q < 4; ++q) {
+      mbar_init(&qfull[q], 1);
+      // consumers of a tile id: the leader's MMA warp, the peer's producer
+      // and the 4 epilogue warps of each CTA
+      mbar_init(&qempty[q], 10);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -626,12 +664,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
 
+  // Tile sequence.  Dynamic (default): the leader's producer takes tiles from
+  // a global counter in raster order and hands each id to both CTAs through
+  // a 4-deep ring (qtile/qfull in each CTA, qempty in the leader), so the
+  // ~74 tiles in flight stay a contiguous window of the L2-aware raster even
+  // when pairs start late (SMs still running K2) or run at different speeds;
+  // a static round-robin assignment let those drifts accumulate over the
+  // ~100 tile waves of the OPT-175B GEMMs and lost the L2 reuse.
+#if ZO2_GEMM2_DYNAMIC
+  auto fetch_tile = [&](uint32_t it) -> uint32_t {  // leader producer (one thread)
+    const int qs = (int)(it & 3u);
+    mbar_wait_cl(&qempty[qs], ((it >> 2) & 1u) ^ 1u);
+    const uint32_t t = atomicAdd(args.tile_ctr, 1u);
+    qtile[qs] = t;
+    st_rank_u32(&qtile[qs], t, 1);
+    mbar_arrive(&qfull[qs]);
+    mbar_arrive_rank(&qfull[qs], 1);
+    return t;
+  };
+  auto take_tile = [&](uint32_t it, bool warp_wide) -> uint32_t {  // every consumer
+    const int qs = (int)(it & 3u);
+    mbar_wait_cl(&qfull[qs], (it >> 2) & 1u);
+    const uint32_t t = qtile[qs];
+    if (warp_wide) __syncwarp();
+    if (!warp_wide || lane == 0) mbar_arrive_rank(&qempty[qs], 0);
+    return t;
+  };
+#endif
+
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (both CTAs)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+#if ZO2_GEMM2_DYNAMIC
+      for (uint32_t it = 0;; ++it) {
+        const uint32_t t = leader ? fetch_tile(it) : take_tile(it, false);
+        if (t >= tiles) break;
+#else
       for (uint32_t t = cid; t < tiles; t += ncl) {
+#endif
         const uint32_t p = t / (tiles_m * tiles_n);
         uint32_t mt, nt;
         tile_mn(t % (tiles_m * tiles_n), tiles_m, tiles_n, args.group_m, mt, nt);
@@ -664,7 +736,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+#if ZO2_GEMM2_DYNAMIC
+      for (uint32_t it = 0;; ++it) {
+        const uint32_t t = take_tile(it, true);
+        if (t >= tiles) break;
+#else
       for (uint32_t t = cid; t < tiles; t += ncl) {
+#endif
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + (uint32_t)(acc * BN);
@@ -705,7 +783,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int quad = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
+#if ZO2_GEMM2_DYNAMIC
+    for (uint32_t it = 0;; ++it) {
+      const uint32_t t = take_tile(it, true);
+      if (t >= tiles) break;
+#else
     for (uint32_t t = cid; t < tiles; t += ncl) {
+#endif
       const uint32_t p = t / (tiles_m * tiles_n);
       uint32_t mt, nt;
       tile_mn(t % (tiles_m * tiles_n), tiles_m, tiles_n, args.group_m, mt, nt);
@@ -723,6 +807,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     }
   }
   __syncthreads();
+#if ZO2_GEMM2_DYNAMIC
+  if (threadIdx.x == 0) {
+    // every leader fetched its last tile id before its CTA got here: the last
+    // CTA out resets the counter pair for the next launch on this slot
+    __threadfence();
+    if (atomicAdd(args.tile_ctr + 1, 1u) == gridDim.x - 1) {
+      atomicExch(args.tile_ctr, 0u);
+      atomicExch(args.tile_ctr + 1, 0u);
+    }
+  }
+#endif
   cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
@@ -796,6 +891,25 @@ int make_map(const void *ptr, uint32_t rows, uint32_t k, uint32_t box_rows, CUte
 int g_num_sms = 0;
 constexpr unsigned kCtrSlots = 256;
 
+// One self-resetting (next tile, CTAs finished) counter pair per launch,
+// rotating over kCtrSlots pairs per device: a pair is reused 256 GEMM
+// launches later, long after the stream-ordered launch that used it ended.
+int tile_counter(unsigned int **out) {
+  static unsigned int *ctrs[64] = {nullptr};
+  static unsigned seq[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return zo2_set_error(ZO2_E_ARG, "zo2_gemm: device id out of range");
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!ctrs[dev]) {
+    cudaError_t e = cudaMalloc(&ctrs[dev], 2 * kCtrSlots * sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMemset(ctrs[dev], 0, 2 * kCtrSlots * sizeof(unsigned int));
+    if (e != cudaSuccess) return zo2_set_cuda_error(e);
+  }
+  *out = ctrs[dev] + 2 * (seq[dev]++ % kCtrSlots);
+  return ZO2_OK;
+}
+
 template <int BN, bool SPLIT, int EPI>
 int launch(const GemmArgs &a, cudaStream_t s) {
   using C = Cfg<BN, SPLIT>;
@@ -814,19 +928,8 @@ int launch(const GemmArgs &a, cudaStream_t s) {
   }
   const uint32_t tiles = ((a.M + BM - 1) / BM) * ((a.N + BN - 1) / BN) * (uint32_t)a.batch;
   const unsigned grid = tiles < (uint32_t)g_num_sms ? tiles : (unsigned)g_num_sms;
-  // one self-resetting counter pair per launch slot (per device)
-  static unsigned int *ctrs[64] = {nullptr};
-  static unsigned seq[64] = {0};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return zo2_set_error(ZO2_E_ARG, "zo2_gemm: device id out of range");
-  if (!ctrs[dev]) {
-    cudaError_t e = cudaMalloc(&ctrs[dev], 2 * kCtrSlots * sizeof(unsigned int));
-    if (e == cudaSuccess) e = cudaMemset(ctrs[dev], 0, 2 * kCtrSlots * sizeof(unsigned int));
-    if (e != cudaSuccess) return zo2_set_cuda_error(e);
-  }
   GemmArgs b = a;
-  b.tile_ctr = ctrs[dev] + 2 * (seq[dev]++ % kCtrSlots);
+  if (int rc = tile_counter(&b.tile_ctr)) return rc;
   b.group_m = g_group_m[0];
   k_gemm<BN, SPLIT, EPI><<<grid, NUM_THREADS, C::SMEM, s>>>(b);
   zo2_count_launch();
@@ -866,6 +969,7 @@ int launch2(const GemmArgs &a, cudaStream_t s) {
       ((a.M + 2 * BM - 1) / (2 * BM)) * ((a.N + C::BN - 1) / C::BN) * (uint32_t)a.batch;
   const uint32_t pairs = tiles < (uint32_t)(g_num_sms / 2) ? tiles : (uint32_t)(g_num_sms / 2);
   GemmArgs b = a;
+  if (int rc = tile_counter(&b.tile_ctr)) return rc;
   b.group_m = g_group_m[1];
   k_gemm2<SPLIT, EPI><<<2 * pairs, NUM_THREADS, C::SMEM, s>>>(b);
   zo2_count_launch();
