@@ -18,7 +18,6 @@ operands load with the same TMA/UMMA 128B-swizzle layout.
 """
 from __future__ import annotations
 
-import ctypes
 import math
 from dataclasses import dataclass
 

@@ -23,7 +23,7 @@ import torch
 
 from . import _lib
 from .errors import CapacityError, SchedulingContractError
-from .model import (EMBED_ID, HEAD_ID, ModelSpec, block_id, init_module_, module_order,
+from .model import (EMBED_ID, HEAD_ID, ModelSpec, block_id, init_module_,
                     module_size)
 from .numerics import CODEC_FORMATS, ConversionSummary, ElemFormat, RngState
 

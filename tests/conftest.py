@@ -4,7 +4,6 @@ Markers: `gpu` tests need a B200 (they call the sm_100a library); everything
 else runs on CPU.  The oracle (oracle/, TEST INFRASTRUCTURE) is the checker.
 """
 import json
-import os
 import sys
 from pathlib import Path
 

@@ -18,7 +18,6 @@ d 12288 / 96 heads (f16 wire); V 50272, S 512, batch 2, two steps + finalize.
 """
 import hashlib
 
-import numpy as np
 import pytest
 import torch
 

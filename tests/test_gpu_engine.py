@@ -12,7 +12,6 @@ Free-running runs (own g) must track the reference within the g tolerance
 """
 import numpy as np
 import pytest
-import torch
 
 pytestmark = pytest.mark.gpu
 

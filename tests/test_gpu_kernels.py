@@ -5,7 +5,6 @@ bit-exact with the oracle (which is pinned to the reference by
 tests/golden).  The GEMM / LayerNorm / attention / CE kernels are floating
 point: tolerances are written per test.
 """
-import ctypes
 
 import numpy as np
 import pytest

@@ -2,7 +2,6 @@
 reference's reproducibility / digest-invariance laws (test_harness.py:158-177)."""
 import csv
 
-import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
