@@ -80,14 +80,21 @@ def peaks():
 # ----------------------------------------------------------------------------
 # clocks sampler (nvidia-smi during the timed region)
 # ----------------------------------------------------------------------------
-# K2 is bound by instruction issue, not HBM: warp instructions per draw from
-# the ncu capture of one OPT-1.3B block (smsp__inst_executed.sum / 2 n draws,
-# profiles/r1_ncu_full_k2_{exact,fast}.txt, n = 50 358 272)
-K2_WARP_INST_PER_DRAW = {"exact": 753229633 / (2 * 50358272),
+# K2 is bound by instruction issue, not HBM: warp instructions per draw
+# (smsp__inst_executed.sum / 2 n draws) from ncu captures of one block:
+#   exact, f32 arena (the queued exact kernel with the certified update draw):
+#     profiles/r2_ncu_full_k2_exact_f32_cfg2_live.txt, OPT-1.3B, n = 50 358 272
+#   exact, codec arena (K2c, the AMP configurations 3-5):
+#     profiles/r2_ncu_full_k2_cert_cfg4_live.txt, OPT-30B, n = 616 562 688
+#   fast z: profiles/r1_ncu_full_k2_fast.txt, OPT-1.3B
+# The blocks are > 97 % of the draws of a step, so the block kernel's figure
+# is the one used.
+K2_WARP_INST_PER_DRAW = {"exact": 659403050 / (2 * 50358272),
+                         "exact_codec": 5385252546 / (2 * 616562688),
                          "fast": 440114924 / (2 * 50358272)}
 
 
-def k2_issue_roofline(draws, ms, rng, clocks, dev):
+def k2_issue_roofline(draws, ms, rng, clocks, dev, codec="none"):
     """K2's roofline: one warp instruction per SM sub-partition per clock at
     the SM clock measured during the run; achieved = draws per second."""
     if not ms:
@@ -95,13 +102,15 @@ def k2_issue_roofline(draws, ms, rng, clocks, dev):
     import torch
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     mhz = (clocks or {}).get("sm_mhz") or 1965.0
-    ipd = K2_WARP_INST_PER_DRAW[rng]
+    key = "exact_codec" if rng == "exact" and codec != "none" else rng
+    ipd = K2_WARP_INST_PER_DRAW[key]
     limit = 4 * sms * mhz * 1e6 / ipd / 1e9
     got = draws / (ms * 1e-3) / 1e9
     return {"bound": "issue", "achieved": got, "peak": limit, "unit": "Gdraws/s",
             "frac": got / limit, "warp_inst_per_draw": ipd, "sm_mhz": mhz,
             "note": "peak = 4 SMSPs x SMs x SM clock / warp instructions per draw "
-                    "(ncu, profiles/r1_ncu_full_k2_*.txt); HBM is ~6% utilised"}
+                    "(ncu captures named at K2_WARP_INST_PER_DRAW in bench.py); HBM is "
+                    "6-8% utilised", "kernel": "K2c (certified)" if key == "exact_codec" else "K2"}
 
 
 class Clocks:
@@ -512,10 +521,15 @@ def run_ours(args, cfg, rank, world, local_rank):
         peak_bf16, peak_src = pk["bf16_tflops_sustained"], pk["source"] + ", sustained"
     else:  # the step's GEMMs beat the 4 s cuBLAS sustained figure: burst binds
         peak_bf16, peak_src = pk["bf16_tflops"], pk["source"] + ", burst (sustained exceeded)"
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "r1_gemm_traffic.json")
-    if split and os.path.exists(tp):
-        traffic = json.load(open(tp))["dram_bytes_per_launch"]
+    traffic, traffic_note = None, None
+    tp = os.path.join(ROOT, "profiles", "r2_gemm_traffic.json")
+    if os.path.exists(tp):
+        tr = json.load(open(tp)).get(args.config)
+        if tr:
+            traffic = tr["dram_bytes"]
+            traffic_note = (f"DRAM bytes of one {tr['kernel']} launch (ncu, {tr['source']}); "
+                            f"algorithmic {tr['algorithmic_bytes'] / 1e9:.2f} GB "
+                            f"({tr['ratio']:.1f}x)")
     line = {
         "metric": "ZO step tokens/s", "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -540,9 +554,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "unit": "TFLOP/s", "frac": (gemm_tflops * passes / peak_bf16
                                                  if gemm_tflops else None),
                      "traffic": traffic,
-                     "traffic_note": ("DRAM bytes of one mlp_out launch (both signs), "
-                                      "profiles/r1_gemm_traffic.json; algorithmic 0.94 GB"
-                                      if traffic else None),
+                     "traffic_note": traffic_note,
                      "peak_source": peak_src + (f", / {passes} tensor passes" if passes > 1 else ""),
                      "algorithmic": "2*M*N*K per GEMM, summed over the step's GEMM launches "
                                     "(CUDA events on the compute stream)",
@@ -553,7 +565,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "gemm_ms_per_step": gemm_ms / args.steps,
                      "k2_ms_per_step": k2_ms / args.steps,
                      "k2_gdraws_per_s": (k2_draws / (k2_ms * 1e-3) / 1e9) if k2_ms else None,
-                     "k2": k2_issue_roofline(k2_draws, k2_ms, args.rng, clk.summary(), dev)},
+                     "k2": k2_issue_roofline(k2_draws, k2_ms, args.rng, clk.summary(), dev,
+                                            cfg["codec"])},
         "step_roofline": {"bound": "pcie" if (t_link or 0) >= t_tensor else "tensor",
                           "link_probe_gbs": {"h2d": probe_up, "d2h": probe_dn,
                                              "note": "1 GiB pinned copies, both directions "
