@@ -25,7 +25,7 @@ arith = os.environ.get("SAN_ARITH", "bf16")
 steps = int(os.environ.get("SAN_STEPS", "2"))
 V = int(os.environ.get("SAN_VOCAB", "50272"))
 codec = "bf16" if arith == "bf16" else None
-spec = ModelSpec(nb, d, d // 128, V, 512)
+spec = ModelSpec(nb, d, d // 128 if d >= 4096 else d // 64, V, 512)
 params = init_params(spec, RngState(5), codec=codec, device=torch.device("cuda", 0))
 rt = OffloadRuntime(params, k_slots=3, codec=codec)
 eng = Zo2Engine(TransformerWorkload(params, arith), ZOConfig(1e-3, 1e-5, steps, 5), rt,
