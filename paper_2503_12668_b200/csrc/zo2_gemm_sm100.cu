@@ -1035,9 +1035,6 @@ __device__ __forceinline__ float ex2f(float x) {
   return y;
 }
 
-#ifndef ZO2_ATT_SB2
-#define ZO2_ATT_SB2 0  // 1: two S/P buffers at every head size (A/B)
-#endif
 template <int HD, bool SPLIT>
 struct AttnTcCfg {
   static constexpr int PL = SPLIT ? 2 : 1;               // planes
@@ -1050,12 +1047,10 @@ struct AttnTcCfg {
   static constexpr int KV_OFF = Q_OFF + PL * PAN * QTILE;  // stage s: K at +2s*KV, V at +(2s+1)*KV
   static constexpr int BAR_OFF = KV_OFF + NS * 2 * KV;
   static constexpr int SMEM = BAR_OFF + 256 + 6 * 128 * 4 + 1024;
-  // TMEM columns (256 per CTA, two CTAs per SM): SB S buffers of 64 columns,
+  // TMEM columns (256 per CTA, two CTAs per SM): two S buffers of 64 columns,
   // then O.  P(g) (bf16 pairs: hi in columns 0-31, lo in 32-63) overwrites
-  // S(g) in its own buffer, so P is buffered along with S.  hd 64 leaves room
-  // for three buffers (S(g+1), S(g+2) can be issued while the softmax of g
-  // runs); hd 128 for two.
-  static constexpr int SB = HD == 64 && !ZO2_ATT_SB2 ? 3 : 2;
+  // S(g) in its own buffer, so P is double-buffered along with S.
+  static constexpr int SB = 2;
   static constexpr uint32_t T_O = SB * ATT_K;
   static constexpr uint32_t TMEM_COLS = 256;
   static_assert(T_O + HD <= TMEM_COLS, "TMEM budget");
@@ -1103,8 +1098,8 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
   uint64_t *bar_kv = (uint64_t *)(smem + C::BAR_OFF);  // [NS] tile loaded (TMA)
   uint64_t *bar_s = bar_kv + NS;                       // [SB] S written (MMA commit)
   uint64_t *bar_p = bar_s + SB;                        // [SB] P written into its S buffer (256 arrivals)
-  uint64_t *bar_pv = bar_p + SB;                       // [SB] P.V(g) done (MMA commit)
-  uint64_t *bar_kvfree = bar_pv + SB;                  // [NS] ring stage read by its MMAs
+  uint64_t *bar_o = bar_p + SB;                        // P.V done (MMA commit)
+  uint64_t *bar_kvfree = bar_o + 1;                    // [NS] ring stage read by its MMAs
   uint64_t *bar_done = bar_kvfree + NS;                // every P.V done (one phase)
   uint32_t *tmem_slot = (uint32_t *)(bar_done + 1);
   float *xch = (float *)(smem + C::BAR_OFF + 256);     // [2][2][128] row max, then [2][128] row sum
@@ -1121,7 +1116,7 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
       mbar_init(&bar_s[i], 1);
       mbar_init(&bar_p[i], ATT_SOFT);
     }
-    for (int i = 0; i < SB; ++i) mbar_init(&bar_pv[i], 1);
+    mbar_init(bar_o, 1);
     for (int i = 0; i < NS; ++i) mbar_init(&bar_kvfree[i], 1);
     mbar_init(bar_done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1144,16 +1139,16 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
 
   // Barrier phases.  Every wait below is on a phase that cannot be two ahead
   // of it (a parity wait trailing its barrier by two phases would hang):
-  //   bar_s[g%SB] phase g/SB: S(g+SB) is issued only after P.V(g) completed,
+  //   bar_s[g%2] phase g/2: S(g+2) is issued only after P.V(g) completed,
   //     which needs P(g), which the softmax writes after reading S(g);
-  //   bar_p[g%SB] phase g/SB: P(g+SB) needs S(g+SB), issued after the MMA
-  //     thread saw P(g) (P.V(g) issued) and P.V(g) completed;
-  //   bar_pv[g%SB] phase g/SB (P.V(g) done), waited before S(g+SB) (MMA
-  //     thread) and at tile g+1 (softmax, only to rescale O): the next phase,
-  //     P.V(g+SB), needs S(g+SB) and P(g+SB), neither possible before those
-  //     waits return.  Each phase is observed by the MMA thread before the
-  //     barrier's next commit (synccheck: no "missing wait").  The epilogue
-  //     waits for bar_done, committed once after the last P.V.
+  //   bar_p[g%2] phase g/2: P(g+2) needs S(g+2), issued after the MMA thread
+  //     saw P(g) (P.V(g) issued) and P.V(g) completed;
+  //   bar_o phase j, waited at tile j+1 (softmax, only to rescale O) and
+  //     before S(j+2) (MMA thread): P.V(j-1) is complete by then (S(j+1)
+  //     waited for it) and P.V(j+1) needs P(j+1), not yet written.  The
+  //     epilogue cannot wait on bar_o (P.V(n-2) may still run, so a parity
+  //     wait for phase n-1 could be satisfied by phase n-3): it waits for
+  //     bar_done, committed once after the last P.V.
   if (warp == ATT_SOFT / 32) {
     // ================================================ TMA + MMA issue (one thread)
     if (lane == 0) {
@@ -1211,7 +1206,7 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
             tc_mma_ts(t_o, pa + ATT_K / 2, vb, id, 1u);
           }
         }
-        tc_commit(&bar_pv[g % SB]);
+        tc_commit(bar_o);
       };
 
       for (uint32_t g = 0; g < (uint32_t)NS && g < n_kt; ++g) load_tile(g);
@@ -1225,13 +1220,19 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
           mbar_wait(&bar_kvfree[gp % NS], (gp / NS) & 1u);
           load_tile(gp + NS);
         }
-        // S(g + 1) next: needs K(g + 1) and its buffer free of P(g + 1 - SB)
+        // S(g + 1) next: needs K(g + 1) and its buffer free of P(g - 1)
         if (g + 1 < n_kt) {
           const uint32_t gn = g + 1;
           mbar_wait(&bar_kv[gn % NS], (gn / NS) & 1u);
-          if (gn >= (uint32_t)SB) mbar_wait(&bar_pv[gn % SB], ((gn - SB) / SB) & 1u);
+          if (gn >= (uint32_t)SB) mbar_wait(bar_o, (gn - SB) & 1u);
           tc_fence_after();
           issue_qk(gn);
+        } else if (g >= 1) {
+          // last tile: observe phase g - 1 of bar_o before committing phase g,
+          // so no phase of the barrier completes unobserved by this thread
+          // (compute-sanitizer synccheck "missing wait"); P.V(g - 1) and P.V(g)
+          // accumulate into the same TMEM columns and serialise anyway
+          mbar_wait(bar_o, (g - 1) & 1u);
         }
         // P.V(g) once the softmax stored P(g)
         mbar_wait(&bar_p[g % SB], (g / SB) & 1u);
@@ -1293,7 +1294,7 @@ __global__ void __launch_bounds__(ATT_SOFT + 32, 2) k_attn_tc(const __grid_const
       // a row's max moved: O(g - 1) must be final before it is rescaled (and
       // P.V(g) is not issued before this warp's P(g) arrives)
       if (g >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
-        mbar_wait(&bar_pv[(g - 1) % SB], ((g - 1) / SB) & 1u);
+        mbar_wait(bar_o, (g - 1) & 1u);
         tc_fence_after();
 #pragma unroll 1
         for (int o0 = half * (HD / 2); o0 < (half + 1) * (HD / 2); o0 += 32) {
