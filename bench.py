@@ -125,10 +125,17 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+        else:
+            # block until the sampler is running (its first line is taken
+            # before the timed region and not counted), so short timed regions
+            # still get samples
+            import select
+            if select.select([self.proc.stdout], [], [], 5.0)[0]:
+                self.proc.stdout.readline()
         return self
 
     def __exit__(self, *a):
@@ -141,6 +148,20 @@ class Clocks:
             f = [x.strip() for x in line.split(",")]
             if len(f) >= 8:
                 self.rows.append(f)
+        self.after = False
+        if not self.rows:
+            # timed region shorter than the sampling interval (cfg1): one
+            # query right after it, flagged as such in the summary
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=10).stdout
+                f = [x.strip() for x in out.strip().split(",")]
+                if len(f) >= 8:
+                    self.rows.append(f)
+                    self.after = True
+            except (OSError, subprocess.SubprocessError):
+                pass
 
     def summary(self):
         if not getattr(self, "rows", None):
@@ -149,9 +170,12 @@ class Clocks:
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        d = {"sm_mhz": statistics.median(sm) if sm else None,
+             "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+             "samples": 0 if getattr(self, "after", False) else len(self.rows)}
+        if getattr(self, "after", False):
+            d["note"] = "timed region shorter than the 100 ms sampling interval: one query right after it"
+        return d
 
 
 # ----------------------------------------------------------------------------
