@@ -411,7 +411,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             from paper_2503_12668_b200.runtime import ResidentRuntime
             rt = ResidentRuntime(params, device=dev)
         else:
-            rt = OffloadRuntime(params, k_slots=cfg["slots"], codec=cfg["codec"],
+            rt = OffloadRuntime(params, k_slots=args.slots or cfg["slots"], codec=cfg["codec"],
                                 capacity_bytes=cfg.get("cap", float("inf")), device=dev)
         eng = Zo2Engine(TransformerWorkload(params, cfg["arith"]),
                         ZOConfig(EPS, cfg["lr"], max(1, args.steps), SEED), rt, validate=True,
@@ -652,6 +652,8 @@ def main():
                     help="z generator: the reference's stream (default) or the fast GPU one")
     ap.add_argument("--no-pipeline", action="store_true",
                     help="per-step device barrier instead of cross-step pipelining")
+    ap.add_argument("--slots", type=int, default=0,
+                    help="device arena slots K (default: the configuration's, 3)")
     ap.add_argument("--gemm-variant", type=int, default=0,
                     help="0 auto (CTA pair for large shapes), 1 single-CTA, 2 pair")
     args = ap.parse_args()
