@@ -146,12 +146,75 @@ class ModelParams:
         """Adopt reference buckets (e.g. zo2lab init_params(...).buckets())."""
         def dev(a):
             return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(device)
-        blocks = []
+        n = module_size(spec, block_id(0))
+        blocks = pinned_blocks(spec.n_blocks, n, torch.float32) if pin else []
         for i in range(spec.n_blocks):
             t = torch.from_numpy(np.ascontiguousarray(flats[block_id(i)], dtype=np.float32))
-            blocks.append(t.pin_memory() if pin else t.clone())
+            if pin:
+                blocks[i].copy_(t)
+            else:
+                blocks.append(t.clone())
         head = flats.get(HEAD_ID, np.zeros(0, np.float32))
         return cls(spec, dev(flats[EMBED_ID]), blocks, dev(head))
+
+
+class _PinnedHostArena:
+    """Page-locked host memory of EXACT size for the block masters: one plain
+    allocation, page-locked with cudaHostRegister (zo2_host_register).
+    torch's pinned allocator rounds every allocation up to a power of two, so
+    a 1.23 GB OPT-30B bf16 block would take 2 GB of host RAM (96 instead of
+    59 GB for the model) -- the difference between fitting and not fitting
+    the masters of a large model, or of N data-parallel ranks, in host RAM.
+    Same DMA rate as cudaHostAlloc (profiles/r2_link_alloc_probe.json).  Every
+    block view carries a reference to the arena, so the range is unregistered
+    only after the last view is gone, just before the memory is freed."""
+
+    HUGE = 1 << 21
+
+    def __init__(self, n_blocks: int, block_elems: int, dtype: torch.dtype):
+        import mmap
+        import os
+        esize = torch.empty((), dtype=dtype).element_size()
+        self.nbytes = n_blocks * block_elems * esize
+        self.registered = False
+        self._map = None
+        mode = os.environ.get("ZO2_HOST_ALLOC", "hugepage")
+        if mode == "torch" or self.nbytes == 0:
+            # torch's pinned allocator (power-of-two rounding), for A/B only
+            self.flat = torch.empty(n_blocks * block_elems, dtype=dtype,
+                                    pin_memory=self.nbytes > 0)
+        else:
+            # anonymous mapping, 2 MB aligned, transparent huge pages where the
+            # kernel grants them: fewer IOMMU / page-table entries per DMA
+            self._map = mmap.mmap(-1, self.nbytes + self.HUGE,
+                                  flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+            if mode == "hugepage" and hasattr(mmap, "MADV_HUGEPAGE"):
+                self._map.madvise(mmap.MADV_HUGEPAGE)
+            raw = torch.frombuffer(self._map, dtype=torch.uint8)
+            off = (-raw.data_ptr()) % self.HUGE
+            self.flat = raw[off:off + self.nbytes].view(dtype)
+            _lib.call("zo2_host_register", self.flat.data_ptr(), self.nbytes)
+            self.registered = True
+        self.ptr = self.flat.data_ptr()
+        self.blocks = []
+        for i in range(n_blocks):
+            b = self.flat[i * block_elems:(i + 1) * block_elems]
+            b._zo2_host_arena = self  # keeps the registration alive with the view
+            self.blocks.append(b)
+
+    def __del__(self):
+        if getattr(self, "registered", False):
+            try:
+                _lib.call("zo2_host_unregister", self.ptr)
+            except Exception:  # noqa: BLE001 -- interpreter shutdown
+                pass
+            self.registered = False
+
+
+def pinned_blocks(n_blocks: int, block_elems: int, dtype: torch.dtype) -> list:
+    """n_blocks page-locked host tensors of block_elems each (one exact-size
+    registered allocation, _PinnedHostArena)."""
+    return _PinnedHostArena(n_blocks, block_elems, dtype).blocks
 
 
 class SharedHostMasters:
@@ -225,6 +288,8 @@ def init_params(spec: ModelSpec, state: RngState, fmt: ElemFormat = ElemFormat.F
     conv = torch.zeros(2, dtype=torch.int64, device=device)
     enc = torch.empty(n, dtype=_TORCH_STORAGE[cfmt], device=device) if cfmt else None
     s = torch.cuda.current_stream().cuda_stream
+    pool = (pinned_blocks(spec.n_blocks, n, dt if cfmt is None else enc.dtype)
+            if pin and host_masters is None else None)
     for i in range(spec.n_blocks):
         if host_masters is not None:
             host = host_masters.blocks[i]
@@ -234,13 +299,13 @@ def init_params(spec: ModelSpec, state: RngState, fmt: ElemFormat = ElemFormat.F
         init_module_(spec, block_id(i), seed, scratch)
         if cfmt is None:
             if host_masters is None:
-                host = torch.empty(n, dtype=dt, pin_memory=pin)
+                host = pool[i] if pool is not None else torch.empty(n, dtype=dt)
             host.copy_(scratch)
         else:
             _lib.call("zo2_encode", scratch.data_ptr(), enc.data_ptr(), cfmt.code, n,
                       conv.data_ptr(), s)
             if host_masters is None:
-                host = torch.empty(n, dtype=enc.dtype, pin_memory=pin)
+                host = pool[i] if pool is not None else torch.empty(n, dtype=enc.dtype)
             host.copy_(enc.view(host.dtype))
         blocks.append(host)
     torch.cuda.synchronize()
@@ -363,11 +428,12 @@ class OffloadRuntime:
             scratch = torch.empty(self.block_size, dtype=torch.float32, device=self.device)
             enc = torch.empty(self.block_size, dtype=sdt, device=self.device)
             s = torch.cuda.current_stream().cuda_stream
+            pool = pinned_blocks(len(self._block_ids), self.block_size, sdt)
             for i, b in enumerate(self._block_ids):
                 scratch.copy_(params.blocks[i])
                 _lib.call("zo2_encode", scratch.data_ptr(), enc.data_ptr(), self.codec.code,
                           self.block_size, self.d_conv.data_ptr(), s)
-                host = torch.empty(self.block_size, dtype=sdt, pin_memory=True)
+                host = pool[i]
                 host.copy_(enc)
                 self.masters[b] = host
             del scratch, enc
