@@ -53,12 +53,13 @@ CONFIGS = {
                  spec=(48, 7168, 56, 50272, 512), B=16, arith="bf16", codec="bf16", lr=1e-7,
                  slots=3, cap=18e9),
     # OPT-175B: the full 96 blocks need 348 GB of pinned fp16 masters; the GPU
-    # boxes of this pool have 196 GB of host RAM, so the bench runs 24 of the 96
-    # full-width blocks and also reports the full-depth step extrapolated from
-    # the measured per-block time (blocks are identical work units)
+    # boxes of this pool have 196 GB of host RAM, so the bench runs 36 of the 96
+    # full-width blocks (130 GB of exact-size page-locked masters) and also
+    # reports the full-depth step extrapolated from the measured per-block
+    # time (blocks are identical work units)
     "cfg5": dict(workload="OPT-175B geometry ZO2 offload, fp16 host masters, bf16 compute, "
-                          "16 x 512, 24 of 96 blocks (host RAM)",
-                 spec=(24, 12288, 96, 50272, 512), B=16, arith="bf16", codec="f16", lr=1e-7,
+                          "16 x 512, 36 of 96 blocks (host RAM)",
+                 spec=(36, 12288, 96, 50272, 512), B=16, arith="bf16", codec="f16", lr=1e-7,
                  slots=3, full_blocks=96),
 }
 EPS, SEED = 1e-3, 1
