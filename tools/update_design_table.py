@@ -6,7 +6,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NAMES = {"cfg1": "cfg1 OPT-125M MeZO f32, resident (no offload), 16×128",
          "cfg2": "cfg2 OPT-1.3B f32, f32 wire", "cfg3": "cfg3 OPT-6.7B bf16, bf16 wire",
          "cfg4": "cfg4 OPT-30B bf16, 18 GB cap",
-         "cfg5": "cfg5 OPT-175B geometry, fp16 wire, 24 of 96 blocks"}
+         "cfg5": "cfg5 OPT-175B geometry, fp16 wire, 36 of 96 blocks"}
 
 
 def fmt(x, nd=0):
@@ -27,7 +27,7 @@ def main(tag="r1"):
         val, ms = fmt(d["value"]), fmt(d["ms_per_step"], 1)
         fe = d.get("full_depth_extrapolation")
         if fe:
-            val += f" (24 blocks) → {fmt(fe['tokens_per_s'])} full depth"
+            val += f" ({fe['blocks_measured']} blocks) → {fmt(fe['tokens_per_s'])} full depth"
             ms += f" → {fmt(fe['step_ms'])}"
         rows.append(f"| {NAMES[base] if rng == 'exact' else base} | {rng} | {val} | {ms} | "
                     f"{r['gemm_ms_per_step']:.1f} | {r['k2_ms_per_step']:.1f} | {r['frac']:.2f} | "
