@@ -227,9 +227,9 @@ int zo2_gemm(const zo2_gemm_problem *probs, int batch, uint32_t M, uint32_t N,
              uint32_t K, int epilogue, void *cuda_stream);
 /* Column width of the CE partials (CE partial count = ceil(N / width)). */
 int zo2_gemm_tile_n(int split);
-/* Kernel choice: 0 auto (CTA-pair cta_group::2 256x256 tiles when M >= 256
- * and N >= 256, else single-CTA 128-row tiles), 1 single-CTA only, 2 pair
- * whenever legal.  For A/B measurements and tests. */
+/* Kernel choice: 0 auto (CTA-pair cta_group::2 256x256 tiles when M >= 256,
+ * N >= 256 and K > 1024, else single-CTA 128-row tiles), 1 single-CTA only,
+ * 2 pair whenever legal.  For A/B measurements and tests. */
 int zo2_set_gemm_variant(int variant);
 /* Tile raster: groups of `group_m` M tiles visited n-major (1 = row-major).
  * Defaults 12 (single-CTA kernel) and 8 (CTA-pair kernel).  For A/B

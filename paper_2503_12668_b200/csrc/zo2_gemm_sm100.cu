@@ -1426,7 +1426,11 @@ extern "C" int zo2_gemm(const zo2_gemm_problem *probs, int batch, uint32_t M, ui
   if (K == 0 || K % 8 != 0) return zo2_set_error(ZO2_E_UNSUPPORTED, "zo2_gemm: K must be a positive multiple of 8");
   const bool split = probs[0].a_lo != nullptr;
   // CTA pair (256 x 256 tiles) for production shapes; single CTA for small ones
-  const bool pair = g_variant != 1 && M >= 2 * BM && N >= 256;
+  // auto: the CTA pair for production shapes; the single-CTA kernel for
+  // K <= 1024 (OPT-125M, cfg1), where a tile's mainloop is too short to
+  // amortise the pair's prologue (measured +1.8 % on the cfg1 step)
+  const bool pair = g_variant == 2 ? (M >= 2 * BM && N >= 256)
+                                   : g_variant != 1 && M >= 2 * BM && N >= 256 && K > 1024;
   const int BROWS = pair ? 128 : (split ? 128 : 256);  // B rows staged per CTA
   GemmArgs a;
   memset(&a, 0, sizeof(a));
