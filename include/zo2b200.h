@@ -232,7 +232,8 @@ int zo2_gemm_tile_n(int split);
  * 2 pair whenever legal.  For A/B measurements and tests. */
 int zo2_set_gemm_variant(int variant);
 /* Tile raster: groups of `group_m` M tiles visited n-major (1 = row-major).
- * Defaults 12 (single-CTA kernel) and 8 (CTA-pair kernel).  For A/B
+ * 0 (default) = automatic: row-major when the whole B operand fits in 80 MB
+ * of L2, else 12 (single-CTA kernel) / 8 (CTA-pair kernel).  For A/B
  * measurements; results do not depend on it. */
 int zo2_set_gemm_raster(int group_m_cta, int group_m_pair);
 

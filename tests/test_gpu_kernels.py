@@ -553,11 +553,11 @@ def test_gemm_raster_invariant(cuda, gemm_variant, split):
     bias = [torch.randn(N, device=cuda) for _ in range(2)]
     outs = {}
     try:
-        for gm in (1, 3, 8, 12, 1024):
+        for gm in (1, 3, 8, 12, 1024, 0):
             L().call("zo2_set_gemm_raster", gm, gm)
             outs[gm] = _run_gemm(A, B, bias, L().EPI_STORE, split)
     finally:
-        L().call("zo2_set_gemm_raster", 12, 8)
+        L().call("zo2_set_gemm_raster", 0, 0)
     for gm, o in outs.items():
         for s in range(2):
             assert torch.equal(o[s], outs[1][s]), (gm, s)

@@ -10,6 +10,9 @@ sys.path.insert(0, ".")
 from paper_2503_12668_b200.model import DualForward, ModelSpec  # noqa: E402
 
 _D = int(os.environ.get("PK_DIM", "2048"))
+if os.environ.get("PK_RASTER"):  # "cta,pair" group heights (zo2_set_gemm_raster)
+    from paper_2503_12668_b200 import _lib as _L
+    _L.call("zo2_set_gemm_raster", *(int(x) for x in os.environ["PK_RASTER"].split(",")))
 _SPEC = (1, _D, _D // 128 if _D >= 4096 else _D // 64, 50272, 512)
 
 
